@@ -1,0 +1,273 @@
+"""Simulated annealing over SASS schedules (reference ``anneal.py``), on the GPU.
+
+``anneal()`` keeps the reference signature and returns an ``AnnealState``
+whose ``history_jsonl()`` is byte-identical to the reference for the same
+seed and a deterministic backend.  Two execution paths, both on the device:
+
+* simulator energy (``SimulatorBackend``, no tester): the complete chain --
+  MT19937 draws, proposal, O(1) legality, scoreboard replay, Metropolis --
+  runs in one kernel launch (``sip_anneal``);
+* any other backend / a tester: *step mode* -- the device draws and vets
+  proposals (``sip_chains_propose``), the host prices each legal candidate
+  with ``backend.measure`` and feeds the time back (``sip_chains_resolve``).
+
+The host only turns the compact per-iteration records into ``HistoryRecord``
+objects (energy = t / t0, feedback = (t_prev - t) / t0, as ``anneal.py:191-193``).
+"""
+from __future__ import annotations
+
+import json
+import math
+from dataclasses import dataclass
+from typing import Callable
+
+import numpy as np
+
+from .backends import MeasurementFailed, SimulatorBackend
+from .engine import (ST_ACCEPTED, ST_MEASURE, ST_PRICED, ST_TEST, STATUS_REASON, get_context,
+                     temperature_schedule)
+from .ir import Kernel
+from .machine import MachineConfig
+from .perturb import NoCandidatesError, candidates
+from .tables import KernelTables
+
+
+class InvalidBaseline(Exception):
+    """Baseline runtime must be strictly positive."""
+
+
+def feedback(t0: float, t_prev: float, t_curr: float) -> float:
+    """Eq. 1 of the paper: (t_prev - t_curr) / t0 (reference anneal.py:28-36)."""
+    if t0 <= 0:
+        raise InvalidBaseline(f"baseline {t0} is not positive")
+    return (t_prev - t_curr) / t0
+
+
+def accept_move(delta_e: float, temperature: float, rng) -> bool:
+    """Metropolis rule (host utility; the device applies the same rule per chain)."""
+    if delta_e < 0:
+        return True
+    return rng.random() < math.exp(-delta_e / temperature)
+
+
+@dataclass(frozen=True)
+class AnnealConfig:
+    t_max: float = 1.0
+    t_min: float = 0.01
+    cooling: float = 1.05
+    seed: int = 0
+    measure_reps: int = 5
+    tests_per_step: int = 0
+    unsafe_moves: bool = False
+    hw_safe: bool = False          # extension; False reproduces the reference
+    min_fixed_distance: int = 12   # hw_safe: issue distance a fixed-latency RAW pair keeps
+
+    def __post_init__(self) -> None:
+        if self.t_min <= 0 or self.t_max <= 0:
+            raise ValueError("temperatures must be positive")
+        if self.t_min > self.t_max:
+            raise ValueError("t_min must not exceed t_max")
+        if self.cooling <= 1.0:
+            raise ValueError("cooling factor must be > 1")
+        if self.measure_reps < 3:
+            raise ValueError("measure_reps must be >= 3")
+        if self.tests_per_step < 0:
+            raise ValueError("tests_per_step must be >= 0")
+
+    @property
+    def iteration_budget(self) -> int:
+        if self.t_max == self.t_min:
+            return 0
+        return math.ceil(math.log(self.t_max / self.t_min) / math.log(self.cooling))
+
+    def temperatures(self) -> np.ndarray:
+        return temperature_schedule(self.t_max, self.cooling, self.iteration_budget)
+
+
+@dataclass(frozen=True)
+class HistoryRecord:
+    iteration: int
+    candidate: int
+    direction: str
+    energy: float | None
+    feedback: float
+    accepted: bool
+    temperature: float
+    rejected: str | None = None
+
+    def to_json(self) -> str:
+        return json.dumps({
+            "iteration": self.iteration,
+            "action": {"candidate": self.candidate, "direction": self.direction},
+            "energy": self.energy,
+            "feedback": self.feedback,
+            "accepted": self.accepted,
+            "temperature": self.temperature,
+            "rejected": self.rejected,
+        }, sort_keys=True)
+
+
+def records_to_history(records, t0: float, temps) -> list:
+    """Compact device records -> HistoryRecord list (energy/feedback as anneal.py:191-193)."""
+    out = []
+    t_prev = t0
+    for it in range(len(records)):
+        r = records[it]
+        st = int(r["status"])
+        direction = "down" if int(r["direction"]) else "up"
+        if st in (ST_ACCEPTED, ST_PRICED):
+            t = float(r["time"])
+            acc = st == ST_ACCEPTED
+            out.append(HistoryRecord(it, int(r["candidate"]), direction, t / t0,
+                                     feedback(t0, t_prev, t), acc, float(temps[it])))
+            if acc:
+                t_prev = t
+        else:
+            out.append(HistoryRecord(it, int(r["candidate"]), direction, None, 0.0, False,
+                                     float(temps[it]), rejected=STATUS_REASON[st]))
+    return out
+
+
+class AnnealState:
+    """Search outcome; ``history`` is materialised lazily from device records."""
+
+    def __init__(self, best: Kernel, best_energy: float, current: Kernel, current_energy: float,
+                 baseline: float, unit: str, iterations: int, history=None, *, records=None,
+                 temps=None, best_perm=None, ambiguous: int = 0):
+        self.best = best
+        self.best_energy = best_energy
+        self.current = current
+        self.current_energy = current_energy
+        self.baseline = baseline
+        self.unit = unit
+        self.iterations = iterations
+        self._history = history
+        self._records = records
+        self._temps = temps
+        self.best_perm = best_perm
+        self.ambiguous = ambiguous
+
+    @property
+    def history(self) -> list:
+        if self._history is None:
+            self._history = ([] if self._records is None
+                             else records_to_history(self._records, self.baseline, self._temps))
+        return self._history
+
+    @property
+    def records(self):
+        return self._records
+
+    @property
+    def best_time(self) -> float:
+        return self.best_energy * self.baseline
+
+    @property
+    def priced(self) -> int:
+        if self._records is None:
+            return sum(1 for r in self.history if r.energy is not None)
+        return int(np.count_nonzero(self._records["status"] <= ST_PRICED))
+
+    def history_jsonl(self) -> str:
+        return "".join(rec.to_json() + "\n" for rec in self.history)
+
+
+def _permuted(kernel: Kernel, perm) -> Kernel:
+    seq = kernel.schedule
+    return kernel.with_schedule(tuple(seq[int(i)] for i in perm))
+
+
+def device_kernel(kernel: Kernel, machine: MachineConfig | None = None, tables: KernelTables | None = None):
+    tables = tables or KernelTables.build(kernel, machine)
+    return get_context().kernel(tables)
+
+
+def anneal_batch_sim(kernel: Kernel, machine: MachineConfig, cfg: AnnealConfig, seeds,
+                     tables: KernelTables | None = None, want_schedules: bool = True) -> list:
+    """Many simulator-energy chains in one launch; one AnnealState per seed."""
+    if len(candidates(kernel)) == 0:
+        raise NoCandidatesError("no global-memory instructions to move")
+    dk = device_kernel(kernel, machine, tables)
+    temps = cfg.temperatures()
+    hist, best, cur, summ = dk.anneal(seeds, temps, cfg.unsafe_moves, cfg.hw_safe,
+                                      cfg.min_fixed_distance, want_schedules=want_schedules)
+    out = []
+    for c in range(len(seeds)):
+        t0 = float(summ["t0"][c])
+        if t0 <= 0:
+            raise InvalidBaseline(f"baseline measurement {t0} is not positive")
+        bk = _permuted(kernel, best[c]) if want_schedules else None
+        ck = _permuted(kernel, cur[c]) if want_schedules else None
+        out.append(AnnealState(bk, float(summ["best_energy"][c]), ck,
+                               float(summ["current_energy"][c]), t0, "cycles", len(temps),
+                               records=hist[c], temps=temps,
+                               best_perm=None if best is None else best[c],
+                               ambiguous=int(summ["ambiguous"][c])))
+    return out
+
+
+def anneal_steps(kernel: Kernel, backend, cfg: AnnealConfig, seeds, *,
+                 tester: Callable[[Kernel], bool] | None = None,
+                 tables: KernelTables | None = None, on_epoch=None) -> list:
+    """Step mode: device proposals, host pricing through ``backend.measure``.
+
+    All chains advance together; each round prices at most one candidate per
+    chain.  ``on_epoch(chains, round)`` may exchange schedules between rounds.
+    """
+    if len(candidates(kernel)) == 0:
+        raise NoCandidatesError("no global-memory instructions to move")
+    seeds = list(seeds)
+    t0 = []
+    for _ in seeds:
+        v = backend.measure(kernel, cfg.measure_reps).value
+        if v <= 0:
+            raise InvalidBaseline(f"baseline measurement {v} is not positive")
+        t0.append(v)
+    dk = device_kernel(kernel, MachineConfig(), tables)
+    temps = cfg.temperatures()
+    chains = dk.chains(seeds, t0, temps, cfg.unsafe_moves, cfg.hw_safe, cfg.min_fixed_distance)
+    C = len(seeds)
+    times = np.zeros(C, dtype=np.float64)
+    status = np.zeros(C, dtype=np.uint8)
+    rnd = 0
+    while True:
+        lo, cand = chains.propose(with_schedules=True)
+        live = np.nonzero(lo >= 0)[0]
+        if len(live) == 0:
+            break
+        for c in live:
+            cand_kernel = _permuted(kernel, cand[c])
+            if tester is not None and not tester(cand_kernel):
+                status[c], times[c] = ST_TEST, 0.0
+                continue
+            try:
+                times[c] = backend.measure(cand_kernel, cfg.measure_reps).value
+                status[c] = ST_PRICED
+            except MeasurementFailed:
+                status[c], times[c] = ST_MEASURE, 0.0
+        chains.resolve(times, status)
+        rnd += 1
+        if on_epoch is not None:
+            on_epoch(chains, rnd)
+    hist, best, cur, summ = chains.result()
+    unit = getattr(backend, "unit", "")
+    return [AnnealState(_permuted(kernel, best[c]), float(summ["best_energy"][c]),
+                        _permuted(kernel, cur[c]), float(summ["current_energy"][c]), t0[c], unit,
+                        len(temps), records=hist[c], temps=temps, best_perm=best[c],
+                        ambiguous=int(summ["ambiguous"][c]))
+            for c in range(C)]
+
+
+def uses_device_energy(backend) -> bool:
+    """True when pricing is the stock scoreboard and may run entirely on the GPU."""
+    return (getattr(backend, "device_energy", False)
+            and type(backend).measure is SimulatorBackend.measure)
+
+
+def anneal(kernel: Kernel, backend, config: AnnealConfig | None = None, *,
+           tester: Callable[[Kernel], bool] | None = None) -> AnnealState:
+    """One annealing chain (reference anneal.py:123-213), executed on the GPU."""
+    cfg = config or AnnealConfig()
+    if uses_device_energy(backend) and tester is None:
+        return anneal_batch_sim(kernel, backend.machine, cfg, [cfg.seed])[0]
+    return anneal_steps(kernel, backend, cfg, [cfg.seed], tester=tester)[0]

@@ -1,0 +1,92 @@
+"""Build libsip.so (sm_100a) and the target cubins in-tree.
+
+    python -m paper_2403_16863_b200.build
+
+nvcc cross-compiles without a GPU, so this runs in the CPU container; the
+resulting .so / .cubin files travel to the GPU box with the repo snapshot.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+TARGETS = PKG / "targets"
+LIB = PKG / "libsip.so"
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
+
+LIB_SOURCES = ["context.cu", "engine.cu", "evaluator.cu", "verify.cu", "targets_launch.cu"]
+CUBINS = {"gemm_lrelu": "gemm_lrelu.cu", "attn_fwd": "attn_fwd.cu"}
+
+
+def _run(cmd, cwd=None) -> None:
+    res = subprocess.run(cmd, cwd=cwd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError(f"command failed: {' '.join(map(str, cmd))}")
+
+
+def _stale(out: Path, deps) -> bool:
+    if not out.exists():
+        return True
+    t = out.stat().st_mtime
+    return any(Path(d).stat().st_mtime > t for d in deps)
+
+
+def build_lib(force: bool = False) -> Path:
+    srcs = [CSRC / s for s in LIB_SOURCES if (CSRC / s).exists()]
+    deps = srcs + list(CSRC.glob("*.h")) + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "sip.h"]
+    if not force and not _stale(LIB, deps):
+        return LIB
+    objdir = PKG / "_obj"
+    objdir.mkdir(exist_ok=True)
+    objs = []
+    for s in srcs:
+        o = objdir / (s.stem + ".o")
+        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+              "-I", str(ROOT / "include"), "-c", str(s),
+              "-o", str(o)])
+        objs.append(str(o))
+    _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *objs, "-ldl", "-lpthread",
+          "-lrt"])
+    return LIB
+
+
+def build_cubins(force: bool = False) -> dict:
+    out = {}
+    for name, src in CUBINS.items():
+        s = TARGETS / src
+        if not s.exists():
+            continue
+        cub = TARGETS / f"{name}.cubin"
+        deps = [s] + list(TARGETS.glob("*.cuh"))
+        if force or _stale(cub, deps):
+            _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-cubin", "-o", str(cub), str(s)])
+        out[name] = cub
+    return out
+
+
+def build_oracle() -> Path | None:
+    """The CPU checker (oracle/), test infrastructure only."""
+    od = ROOT / "oracle"
+    if not (od / "Makefile").exists():
+        return None
+    _run(["make", "-s", "-C", str(od)])
+    return od / "_build" / "libsip_oracle.so"
+
+
+def build_all(force: bool = False) -> None:
+    build_lib(force)
+    build_cubins(force)
+    build_oracle()
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv)
+    print(f"built {LIB}")

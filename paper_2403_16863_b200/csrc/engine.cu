@@ -1,0 +1,922 @@
+// engine.cu -- G1 pair-legality matrix, G2 batched annealing chains and the
+// scoreboard replay, for sm_100a.
+//
+// Reference hot loop (pure Python, one chain at a time):
+//   anneal.anneal            anneal.py:123-213
+//   perturb.sample_action    perturb.py:56-61
+//   perturb.apply_action     perturb.py:64-90   (graph.connected, deps.py:50-53)
+//   deps.build_depgraph      deps.py:279-349    (rebuilt after every accept)
+//   machine.simulate         machine.py:116-161
+// Here a chain is one thread; thousands of chains run per launch.  Legality is
+// O(1) per proposal: one bit of the E matrix built once per listing (G1), so
+// no graph is ever rebuilt.  Per-chain state is stored position-major
+// ([n][chains]) so a warp's 32 chains touch one line per position.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "common.h"
+#include "rng.cuh"
+
+namespace sip {
+
+int fail(sip_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+constexpr uint32_t FENCE_BIT = 1u << 21;
+constexpr uint32_t GLOBAL_BIT = 1u << 22;
+
+__host__ __device__ __forceinline__ uint32_t c_wait(uint32_t c) { return c & 63u; }
+__host__ __device__ __forceinline__ uint32_t c_rd(uint32_t c) { return (c >> 6) & 7u; }
+__host__ __device__ __forceinline__ uint32_t c_wr(uint32_t c) { return (c >> 9) & 7u; }
+__host__ __device__ __forceinline__ uint32_t c_adv(uint32_t c) { return (c >> 12) & 31u; }
+__host__ __device__ __forceinline__ uint32_t c_reuse(uint32_t c) { return (c >> 17) & 15u; }
+__host__ __device__ __forceinline__ uint32_t c_sets(uint32_t c) {
+  uint32_t rd = c_rd(c), wr = c_wr(c);
+  return (rd < 6 ? 1u << rd : 0u) | (wr < 6 ? 1u << wr : 0u);
+}
+
+// ---------------------------------------------------------------------------
+// G1: E(a, b) -- must ordering edge join a (first) and b (second)?
+// Derivation: for adjacent slots, build_depgraph's last-writer /
+// readers-since / last-setter / waiters-since bookkeeping reduces to a pure
+// function of the two instructions.
+__device__ bool mem_alias(const sip_memref& x, const sip_memref& y) {
+  if (x.space != 3 && y.space != 3 && x.space != y.space) return false;  // deps.py:250-251
+  if (x.base < 0 || y.base < 0 || x.base != y.base) return true;         // deps.py:252-255
+  return x.offset < y.offset + y.size && y.offset < x.offset + x.size;   // deps.py:256
+}
+
+__device__ bool pair_edge(const KernelDev d, int a, int b) {
+  uint32_t ca = d.meta[a].x, cb = d.meta[b].x;
+  if ((ca | cb) & FENCE_BIT) return true;  // BLOCK_FENCE, deps.py:336-343
+  const uint64_t* ra = d.reads + (size_t)a * d.words;
+  const uint64_t* wa = d.writes + (size_t)a * d.words;
+  const uint64_t* rb = d.reads + (size_t)b * d.words;
+  const uint64_t* wb = d.writes + (size_t)b * d.words;
+  for (int w = 0; w < d.words; ++w) {  // RAW | WAR | WAW, deps.py:298-312
+    uint64_t WA = wa[w], WB = wb[w];
+    if ((WA & rb[w]) | (ra[w] & WB) | (WA & WB)) return true;
+  }
+  uint32_t sa = c_sets(ca), sb = c_sets(cb);
+  if (sa & c_wait(cb)) return true;                 // setter -> waiter, deps.py:316-319
+  if ((c_wait(ca) & ~sa) & sb) return true;         // waiter -> next setter, deps.py:320-326
+  int na = d.nrefs[a], nb = d.nrefs[b];             // memory order, deps.py:263-276,328-334
+  if (na && nb) {
+    bool both_global = (ca & GLOBAL_BIT) && (cb & GLOBAL_BIT);
+    for (int i = 0; i < na; ++i) {
+      sip_memref x = d.refs[a * SIP_MAX_REFS + i];
+      for (int j = 0; j < nb; ++j) {
+        sip_memref y = d.refs[b * SIP_MAX_REFS + j];
+        if (mem_alias(x, y) && (x.write || y.write || both_global)) return true;
+      }
+    }
+  }
+  return false;
+}
+
+// one warp per (global instruction g, 32-identity word): ballot the row bits
+__global__ void legality_build_kernel(KernelDev d) {
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  int g = blockIdx.y;
+  if (warp >= d.nw32) return;
+  int x = warp * 32 + lane;
+  int me = d.gids[g];
+  bool after = false, before = false;
+  if (x < d.n) {
+    after = pair_edge(d, me, x);
+    before = pair_edge(d, x, me);
+  }
+  uint32_t wa = __ballot_sync(0xffffffffu, after);
+  uint32_t wb = __ballot_sync(0xffffffffu, before);
+  if (lane == 0) {
+    d.e_after[(size_t)g * d.nw32 + warp] = wa;
+    d.e_before[(size_t)g * d.nw32 + warp] = wb;
+  }
+}
+
+__device__ __forceinline__ bool edge_lookup(const KernelDev& d, const int16_t* gid, int a, int b) {
+  int ga = gid[a];
+  if (ga >= 0) return (__ldg(d.e_after + (size_t)ga * d.nw32 + (b >> 5)) >> (b & 31)) & 1u;
+  int gb = gid[b];
+  return (__ldg(d.e_before + (size_t)gb * d.nw32 + (a >> 5)) >> (a & 31)) & 1u;
+}
+
+// ---------------------------------------------------------------------------
+// Hardware-safety extension (off in parity mode).  The
+// reference ignores fixed-latency issue distance and operand reuse
+// (SURVEY K8); on real sm_100a these decide correctness.
+__device__ bool regs_overlap(const KernelDev& d, int p, int q) {
+  // W(p) intersects R(q) u W(q)
+  const uint64_t* wp = d.writes + (size_t)p * d.words;
+  const uint64_t* rq = d.reads + (size_t)q * d.words;
+  const uint64_t* wq = d.writes + (size_t)q * d.words;
+  for (int w = 0; w < d.words; ++w)
+    if (wp[w] & (rq[w] | wq[w])) return true;
+  return false;
+}
+
+template <typename SchedAt>
+__device__ bool hw_safe_ok(const KernelDev& d, const uint2* meta, SchedAt at, int n, int lo, int a,
+                           int b, int minfix) {
+  if (d.pin[a] || d.pin[b]) return false;
+  if (c_reuse(meta[a].x) || c_reuse(meta[b].x)) return false;
+  if (lo > 0 && c_reuse(meta[at(lo - 1)].x)) return false;
+  // producers P above: distance P -> b shrinks by adv(a)
+  uint32_t dist = 0;
+  for (int p = lo - 1; p >= 0; --p) {
+    int x = at(p);
+    dist += c_adv(meta[x].x);
+    if ((int)dist >= minfix) break;
+    if (c_wr(meta[x].x) >= 6 && regs_overlap(d, x, b)) return false;
+    if (d.cut[p]) return false;  // block entry reached inside the window
+  }
+  // consumers Q below: distance a -> Q shrinks by adv(b)
+  bool fixed_a = c_wr(meta[a].x) >= 6;
+  if (fixed_a) {
+    dist = c_adv(meta[a].x);
+    for (int p = lo + 2; p < n && (int)dist < minfix; ++p) {
+      if (d.cut[p]) return false;
+      int x = at(p);
+      if (regs_overlap(d, a, x)) return false;
+      dist += c_adv(meta[x].x);
+    }
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// scoreboard replay (machine.py:116-161)
+struct Sb {
+  int ptr, fin;
+  int clr[6];
+  __device__ __forceinline__ void reset() {
+    ptr = fin = 0;
+#pragma unroll
+    for (int b = 0; b < 6; ++b) clr[b] = 0;
+  }
+  __device__ __forceinline__ void step(uint2 m) {
+    uint32_t c = m.x;
+    int issue = ptr;
+#pragma unroll
+    for (int b = 0; b < 6; ++b)
+      if ((c >> b) & 1u) issue = max(issue, clr[b]);
+    int done = issue + (int)m.y;
+    uint32_t rd = c_rd(c), wr = c_wr(c);
+#pragma unroll
+    for (int b = 0; b < 6; ++b)
+      if (rd == (uint32_t)b || wr == (uint32_t)b) clr[b] = done;
+    fin = max(fin, done);
+    ptr = issue + (int)c_adv(c);
+  }
+  __device__ __forceinline__ int total() const { return max(fin, ptr); }
+};
+
+// total of the chain's schedule with slots (lo, lo+1) exchanged (lo = -1: as is)
+__device__ int sim_swapped(const uint2* meta, const uint16_t* sched, int C, int c, int n, int lo) {
+  Sb s;
+  s.reset();
+  const uint16_t* col = sched + c;
+  int end0 = lo < 0 ? n : lo;
+  for (int p = 0; p < end0; ++p) s.step(meta[col[(size_t)p * C]]);
+  if (lo >= 0) {
+    s.step(meta[col[(size_t)(lo + 1) * C]]);
+    s.step(meta[col[(size_t)lo * C]]);
+    for (int p = lo + 2; p < n; ++p) s.step(meta[col[(size_t)p * C]]);
+  }
+  return s.total();
+}
+
+// ---------------------------------------------------------------------------
+// chain state (device), position-major [*, C]
+struct Chains {
+  int C = 0, n = 0, k = 0, budget = 0;
+  int unsafe = 0, hw_safe = 0, minfix = 0;
+  uint16_t* sched = nullptr;
+  uint16_t* best = nullptr;
+  uint16_t* cpos = nullptr;
+  uint32_t* mt = nullptr;
+  int32_t* mti = nullptr;
+  double* t0 = nullptr;
+  double* e_x = nullptr;
+  double* e_best = nullptr;
+  int32_t* it = nullptr;
+  int32_t* best_iter = nullptr;
+  int32_t* ambiguous = nullptr;
+  int32_t* p_lo = nullptr;
+  uint16_t* p_cand = nullptr;
+  uint8_t* p_dir = nullptr;
+  sip_record* hist = nullptr;
+  const double* temps = nullptr;
+  const int64_t* seeds = nullptr;
+  uint16_t* cand_out = nullptr;  // [C][n] chain-major candidate schedules (step mode)
+};
+
+__device__ __forceinline__ void record(const Chains& s, int c, int it, int status, double t, int lo,
+                                       int cand, int dir) {
+  sip_record r;
+  r.time = t;
+  r.lo = lo;
+  r.candidate = (uint16_t)cand;
+  r.direction = (uint8_t)dir;
+  r.status = (uint8_t)status;
+  s.hist[(size_t)c * s.budget + it] = r;
+}
+
+// perturb.sample_action + apply_action checks.  Returns -1 when the move is
+// legal (lo/cand/dir filled) or the SIP_ST_* rejection reason.
+__device__ int propose(const KernelDev& d, const uint2* meta, const int16_t* gid, const Chains& s,
+                       int c, MtRef& mt, int& cand, int& dir, int& lo) {
+  uint32_t cell = mt_randbelow(mt, 2u * (uint32_t)s.k);
+  cand = (int)(cell >> 1);
+  dir = (int)(cell & 1u);  // 0 = UP
+  int pos = s.cpos[(size_t)cand * s.C + c];
+  lo = dir == 0 ? pos - 1 : pos;
+  if (lo < 0 || lo + 1 >= s.n) return SIP_ST_BOUNDARY;
+  if (d.cut[lo + 1]) return SIP_ST_BOUNDARY;
+  int a = s.sched[(size_t)lo * s.C + c], b = s.sched[(size_t)(lo + 1) * s.C + c];
+  if (!s.unsafe && edge_lookup(d, gid, a, b)) return SIP_ST_DEPENDENCY;
+  if (s.hw_safe) {
+    auto at = [&](int p) { return (int)s.sched[(size_t)p * s.C + c]; };
+    if (!hw_safe_ok(d, meta, at, s.n, lo, a, b, s.minfix)) return SIP_ST_HWSAFE;
+  }
+  return -1;
+}
+
+__device__ void apply_swap(const int16_t* gid, const Chains& s, int c, int lo, int cand, int dir) {
+  uint16_t* x = s.sched + (size_t)lo * s.C + c;
+  uint16_t* y = s.sched + (size_t)(lo + 1) * s.C + c;
+  uint16_t a = *x, b = *y;
+  *x = b;
+  *y = a;
+  int other = dir == 0 ? a : b;  // the neighbour the candidate traded places with
+  if (gid[other] < 0) s.cpos[(size_t)cand * s.C + c] += (dir == 0 ? -1 : 1);
+}
+
+__device__ void copy_best(const Chains& s, int c) {
+  for (int p = 0; p < s.n; ++p) s.best[(size_t)p * s.C + c] = s.sched[(size_t)p * s.C + c];
+}
+
+// Metropolis rule (anneal.py:39-44); counts decisions too close to call.
+__device__ bool metropolis(double delta_e, double temp, MtRef& mt, int& ambiguous) {
+  if (delta_e < 0) return true;
+  double r = mt_random(mt);
+  double p = exp(-delta_e / temp);
+  if (fabs(r - p) <= 4.0 * (nextafter(p, 2.0) - p)) ++ambiguous;
+  return r < p;
+}
+
+// shared-memory staging of (ctrl, lat) and identity -> global-index tables
+struct Staged {
+  const uint2* meta;
+  const int16_t* gid;
+};
+
+__device__ Staged stage_tables(const KernelDev& d, bool use_smem) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (!use_smem) return {d.meta, d.gid};
+  uint2* m = reinterpret_cast<uint2*>(smem_raw);
+  int16_t* g = reinterpret_cast<int16_t*>(smem_raw + sizeof(uint2) * d.n);
+  for (int i = threadIdx.x; i < d.n; i += blockDim.x) {
+    m[i] = d.meta[i];
+    g[i] = d.gid[i];
+  }
+  __syncthreads();
+  return {m, g};
+}
+
+__device__ void chain_init(const KernelDev& d, const Chains& s, int c, const uint32_t* base,
+                           MtRef& mt) {
+  for (int p = 0; p < s.n; ++p) {
+    s.sched[(size_t)p * s.C + c] = (uint16_t)p;
+    s.best[(size_t)p * s.C + c] = (uint16_t)p;
+  }
+  for (int j = 0; j < s.k; ++j) s.cpos[(size_t)j * s.C + c] = (uint16_t)d.gids[j];
+  uint32_t key[2];
+  int klen = mt_key_from_int(s.seeds[c], key);
+  mt_init_by_array(mt, base, key, klen);
+}
+
+// ---- fused simulator-energy annealing: whole chain in one launch ----------
+__global__ void __launch_bounds__(128) anneal_fused_kernel(KernelDev d, Chains s,
+                                                           const uint32_t* mt_base, int use_smem,
+                                                           double t0_cycles) {
+  Staged tb = stage_tables(d, use_smem);
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= s.C) return;
+  MtRef mt{s.mt + c, s.C, MT_N};
+  chain_init(d, s, c, mt_base, mt);
+  const double t0 = t0_cycles;
+  double e_x = 1.0, e_best = 1.0;
+  int best_iter = -1, amb = 0;
+  for (int it = 0; it < s.budget; ++it) {
+    int cand, dir, lo;
+    int st = propose(d, tb.meta, tb.gid, s, c, mt, cand, dir, lo);
+    if (st >= 0) {
+      record(s, c, it, st, 0.0, lo, cand, dir);
+      continue;
+    }
+    double t = (double)sim_swapped(tb.meta, s.sched, s.C, c, s.n, lo);
+    double e_c = t / t0;
+    double de = e_c - e_x;
+    bool acc = metropolis(de, s.temps[it], mt, amb);
+    if (acc) {
+      apply_swap(tb.gid, s, c, lo, cand, dir);
+      e_x = e_c;
+      if (de < 0 && e_c < e_best) {
+        e_best = e_c;
+        best_iter = it;
+        copy_best(s, c);
+      }
+    }
+    record(s, c, it, acc ? SIP_ST_ACCEPTED : SIP_ST_PRICED, t, lo, cand, dir);
+  }
+  s.t0[c] = t0;
+  s.e_x[c] = e_x;
+  s.e_best[c] = e_best;
+  s.best_iter[c] = best_iter;
+  s.ambiguous[c] = amb;
+  s.mti[c] = mt.mti;
+}
+
+// ---- step mode: externally priced candidates -------------------------------
+__global__ void chains_init_kernel(KernelDev d, Chains s, const uint32_t* mt_base,
+                                   const double* t0) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= s.C) return;
+  MtRef mt{s.mt + c, s.C, MT_N};
+  chain_init(d, s, c, mt_base, mt);
+  s.mti[c] = mt.mti;
+  s.t0[c] = t0[c];
+  s.e_x[c] = 1.0;
+  s.e_best[c] = 1.0;
+  s.it[c] = 0;
+  s.best_iter[c] = -1;
+  s.ambiguous[c] = 0;
+  s.p_lo[c] = -1;
+}
+
+__global__ void __launch_bounds__(128) chains_propose_kernel(KernelDev d, Chains s, int use_smem,
+                                                             int32_t* lo_out) {
+  Staged tb = stage_tables(d, use_smem);
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= s.C) return;
+  MtRef mt{s.mt + c, s.C, s.mti[c]};
+  int it = s.it[c];
+  int lo = -1, cand = 0, dir = 0;
+  while (it < s.budget) {
+    int st = propose(d, tb.meta, tb.gid, s, c, mt, cand, dir, lo);
+    if (st < 0) break;
+    record(s, c, it, st, 0.0, lo, cand, dir);
+    ++it;
+    lo = -1;
+  }
+  s.it[c] = it;
+  s.mti[c] = mt.mti;
+  s.p_lo[c] = lo;
+  s.p_cand[c] = (uint16_t)cand;
+  s.p_dir[c] = (uint8_t)dir;
+  lo_out[c] = lo;
+  if (s.cand_out != nullptr && lo >= 0) {
+    uint16_t* out = s.cand_out + (size_t)c * s.n;
+    for (int p = 0; p < s.n; ++p) out[p] = s.sched[(size_t)p * s.C + c];
+    uint16_t t = out[lo];
+    out[lo] = out[lo + 1];
+    out[lo + 1] = t;
+  }
+}
+
+__global__ void chains_resolve_kernel(KernelDev d, Chains s, const double* t_curr,
+                                      const uint8_t* status) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= s.C) return;
+  int lo = s.p_lo[c];
+  if (lo < 0) return;
+  int it = s.it[c];
+  int cand = s.p_cand[c], dir = s.p_dir[c];
+  s.p_lo[c] = -1;
+  s.it[c] = it + 1;
+  int st = status[c];
+  if (st != SIP_ST_PRICED) {
+    record(s, c, it, st, 0.0, lo, cand, dir);
+    return;
+  }
+  MtRef mt{s.mt + c, s.C, s.mti[c]};
+  double t = t_curr[c], t0 = s.t0[c];
+  double e_c = t / t0, e_x = s.e_x[c];
+  double de = e_c - e_x;
+  int amb = s.ambiguous[c];
+  bool acc = metropolis(de, s.temps[it], mt, amb);
+  s.ambiguous[c] = amb;
+  s.mti[c] = mt.mti;
+  if (acc) {
+    apply_swap(d.gid, s, c, lo, cand, dir);
+    s.e_x[c] = e_c;
+    if (de < 0 && e_c < s.e_best[c]) {
+      s.e_best[c] = e_c;
+      s.best_iter[c] = it;
+      copy_best(s, c);
+    }
+  }
+  record(s, c, it, acc ? SIP_ST_ACCEPTED : SIP_ST_PRICED, t, lo, cand, dir);
+}
+
+__global__ void chains_adopt_kernel(KernelDev d, Chains s, const uint16_t* sched, double energy) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= s.C) return;
+  int j = 0;
+  for (int p = 0; p < s.n; ++p) {
+    uint16_t x = sched[p];
+    s.sched[(size_t)p * s.C + c] = x;
+    if (d.gid[x] >= 0) s.cpos[(size_t)(j++) * s.C + c] = (uint16_t)p;
+  }
+  s.e_x[c] = energy;
+}
+
+// ---- API helpers: batch simulate + legality queries ------------------------
+__global__ void simulate_kernel(KernelDev d, const uint16_t* scheds, int count, int64_t* totals,
+                                int32_t* waited, int8_t* binding) {
+  int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= count) return;
+  const uint16_t* sc = scheds + (size_t)q * d.n;
+  Sb s;
+  s.reset();
+  for (int p = 0; p < d.n; ++p) {
+    uint2 m = d.meta[sc[p]];
+    if (waited != nullptr) {
+      int wu = s.ptr, bind = -1;
+      for (int b = 0; b < 6; ++b)
+        if (((m.x >> b) & 1u) && s.clr[b] > wu) {
+          wu = s.clr[b];
+          bind = b;
+        }
+      waited[(size_t)q * d.n + p] = wu - s.ptr;
+      binding[(size_t)q * d.n + p] = (int8_t)bind;
+    }
+    s.step(m);
+  }
+  totals[q] = d.n ? s.total() : 0;
+}
+
+__global__ void legality_query_kernel(KernelDev d, const uint16_t* scheds, const int32_t* los,
+                                      int nq, int hw_safe, int minfix, uint8_t* legal) {
+  int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  const uint16_t* sc = scheds + (size_t)q * d.n;
+  int lo = los[q];
+  bool ok = lo >= 0 && lo + 1 < d.n && !d.cut[lo + 1];
+  if (ok) {
+    int a = sc[lo], b = sc[lo + 1];
+    if (d.gid[a] < 0 && d.gid[b] < 0) {
+      ok = !pair_edge(d, a, b);  // neither is a candidate: evaluate E directly
+    } else {
+      ok = !edge_lookup(d, d.gid, a, b);
+    }
+    if (ok && hw_safe) {
+      auto at = [&](int p) { return (int)sc[p]; };
+      ok = hw_safe_ok(d, d.meta, at, d.n, lo, a, b, minfix);
+    }
+  }
+  legal[q] = ok ? 1 : 0;
+}
+
+// ---------------------------------------------------------------------------
+static std::vector<uint32_t> g_mt_base;  // init_genrand(19650218), shared by all chains
+
+static const std::vector<uint32_t>& mt_base_host() {
+  if (g_mt_base.empty()) {
+    g_mt_base.resize(MT_N);
+    MtRef m{g_mt_base.data(), 1, 0};
+    mt_init_genrand(m, 19650218u);
+  }
+  return g_mt_base;
+}
+
+template <typename T>
+static int dalloc(sip_ctx* ctx, T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  SIP_CUDA(ctx, cudaMalloc((void**)p, sizeof(T) * count));
+  return SIP_OK;
+}
+
+template <typename T>
+static int h2d(sip_ctx* ctx, T* dst, const T* src, size_t count) {
+  if (count == 0) return SIP_OK;
+  SIP_CUDA(ctx, cudaMemcpyAsync(dst, src, sizeof(T) * count, cudaMemcpyHostToDevice, ctx->stream));
+  return SIP_OK;
+}
+
+template <typename T>
+static int d2h(sip_ctx* ctx, T* dst, const T* src, size_t count) {
+  if (count == 0) return SIP_OK;
+  SIP_CUDA(ctx, cudaMemcpyAsync(dst, src, sizeof(T) * count, cudaMemcpyDeviceToHost, ctx->stream));
+  return SIP_OK;
+}
+
+#define TRY(x)                  \
+  do {                          \
+    int rc_ = (x);              \
+    if (rc_ != SIP_OK) return rc_; \
+  } while (0)
+
+static size_t smem_need(const KernelDev& d) { return (sizeof(uint2) + sizeof(int16_t)) * d.n + 16; }
+
+static int configure_smem(sip_ctx* ctx, const void* fn, size_t bytes) {
+  SIP_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  return SIP_OK;
+}
+
+static constexpr size_t kSmemCap = 200 * 1024;
+
+}  // namespace sip
+
+using namespace sip;
+
+struct sip_chains {
+  sip_kernel* k = nullptr;
+  Chains s;
+  std::vector<double> temps;
+  double* d_temps = nullptr;
+  int64_t* d_seeds = nullptr;
+  double* d_tcurr = nullptr;
+  uint8_t* d_status = nullptr;
+  int32_t* d_lo = nullptr;
+  uint16_t* d_adopt = nullptr;
+};
+
+static int chains_alloc(sip_ctx* ctx, sip_kernel* k, const sip_anneal_cfg* cfg, int chains,
+                        const int64_t* seeds, sip_chains* o) {
+  Chains& s = o->s;
+  s.C = chains;
+  s.n = k->d.n;
+  s.k = k->d.k;
+  s.budget = cfg->budget;
+  s.unsafe = cfg->unsafe_moves;
+  s.hw_safe = cfg->hw_safe;
+  s.minfix = cfg->min_fixed_distance;
+  size_t C = chains, n = s.n;
+  TRY(dalloc(ctx, &s.sched, n * C));
+  TRY(dalloc(ctx, &s.best, n * C));
+  TRY(dalloc(ctx, &s.cpos, (size_t)std::max(s.k, 1) * C));
+  TRY(dalloc(ctx, &s.mt, (size_t)MT_N * C));
+  TRY(dalloc(ctx, &s.mti, C));
+  TRY(dalloc(ctx, &s.t0, C));
+  TRY(dalloc(ctx, &s.e_x, C));
+  TRY(dalloc(ctx, &s.e_best, C));
+  TRY(dalloc(ctx, &s.it, C));
+  TRY(dalloc(ctx, &s.best_iter, C));
+  TRY(dalloc(ctx, &s.ambiguous, C));
+  TRY(dalloc(ctx, &s.p_lo, C));
+  TRY(dalloc(ctx, &s.p_cand, C));
+  TRY(dalloc(ctx, &s.p_dir, C));
+  TRY(dalloc(ctx, &s.hist, (size_t)std::max(s.budget, 1) * C));
+  TRY(dalloc(ctx, &o->d_temps, (size_t)std::max(s.budget, 1)));
+  TRY(dalloc(ctx, &o->d_seeds, C));
+  TRY(h2d(ctx, o->d_temps, cfg->temperature, (size_t)s.budget));
+  TRY(h2d(ctx, o->d_seeds, seeds, C));
+  s.temps = o->d_temps;
+  s.seeds = o->d_seeds;
+  return SIP_OK;
+}
+
+static void chains_free(sip_chains* o) {
+  Chains& s = o->s;
+  void* ptrs[] = {s.sched, s.best, s.cpos, s.mt, s.mti, s.t0, s.e_x, s.e_best, s.it,
+                  s.best_iter, s.ambiguous, s.p_lo, s.p_cand, s.p_dir, s.hist, o->d_temps,
+                  o->d_seeds, o->d_tcurr, o->d_status, o->d_lo, s.cand_out, o->d_adopt};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+}
+
+// transpose position-major [n][C] device array into chain-major host [C][n]
+static int fetch_sched(sip_ctx* ctx, const uint16_t* dsrc, int n, int C, uint16_t* host) {
+  std::vector<uint16_t> tmp((size_t)n * C);
+  TRY(d2h(ctx, tmp.data(), dsrc, tmp.size()));
+  SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  for (int p = 0; p < n; ++p)
+    for (int c = 0; c < C; ++c) host[(size_t)c * n + p] = tmp[(size_t)p * C + c];
+  return SIP_OK;
+}
+
+static int chains_fetch(sip_chains* o, sip_record* history, uint16_t* best, uint16_t* current,
+                        sip_chain_summary* summary) {
+  sip_ctx* ctx = o->k->ctx;
+  Chains& s = o->s;
+  size_t C = s.C;
+  if (history) TRY(d2h(ctx, history, s.hist, C * s.budget));
+  if (best) TRY(fetch_sched(ctx, s.best, s.n, s.C, best));
+  if (current) TRY(fetch_sched(ctx, s.sched, s.n, s.C, current));
+  if (summary) {
+    std::vector<double> t0(C), ex(C), eb(C);
+    std::vector<int32_t> bi(C), am(C);
+    TRY(d2h(ctx, t0.data(), s.t0, C));
+    TRY(d2h(ctx, ex.data(), s.e_x, C));
+    TRY(d2h(ctx, eb.data(), s.e_best, C));
+    TRY(d2h(ctx, bi.data(), s.best_iter, C));
+    TRY(d2h(ctx, am.data(), s.ambiguous, C));
+    SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    for (size_t c = 0; c < C; ++c)
+      summary[c] = sip_chain_summary{t0[c], eb[c], ex[c], bi[c], am[c]};
+  }
+  SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return SIP_OK;
+}
+
+extern "C" {
+
+const char* sip_version(void) { return "sip-b200 0.1.0 (sm_100a)"; }
+
+int sip_device_count(int* count) {
+  if (!count) return SIP_E_ARG;
+  cudaError_t e = cudaGetDeviceCount(count);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return SIP_E_CUDA;
+  }
+  return SIP_OK;
+}
+
+const char* sip_last_error(sip_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int sip_kernel_create(sip_ctx* ctx, const sip_tables* t, sip_kernel** out) {
+  if (!ctx || !t || !out) return SIP_E_ARG;
+  if (t->n < 1 || t->n > 65535 || t->words < 1) return fail(ctx, SIP_E_ARG, "listing size out of range");
+  SIP_CUDA(ctx, cudaSetDevice(ctx->device));
+  auto* k = new sip_kernel();
+  k->ctx = ctx;
+  KernelDev& d = k->d;
+  d.n = t->n;
+  d.words = t->words;
+  d.nw32 = (t->n + 31) / 32;
+  size_t n = d.n;
+  std::vector<uint2> meta(n);
+  std::vector<int16_t> gid(n, -1);
+  std::vector<int32_t> gids;
+  for (size_t i = 0; i < n; ++i) {
+    meta[i] = make_uint2(t->ctrl[i], t->lat[i]);
+    if (t->ctrl[i] & GLOBAL_BIT) {
+      gid[i] = (int16_t)gids.size();
+      gids.push_back((int32_t)i);
+    }
+  }
+  d.k = (int)gids.size();
+  std::vector<uint8_t> pin(n, 0);
+  if (t->pin) std::memcpy(pin.data(), t->pin, n);
+  int rc = SIP_OK;
+  if ((rc = dalloc(ctx, &d.meta, n)) || (rc = dalloc(ctx, &d.klass, n)) ||
+      (rc = dalloc(ctx, &d.reads, n * d.words)) || (rc = dalloc(ctx, &d.writes, n * d.words)) ||
+      (rc = dalloc(ctx, &d.refs, n * SIP_MAX_REFS)) || (rc = dalloc(ctx, &d.nrefs, n)) ||
+      (rc = dalloc(ctx, &d.cut, n + 1)) || (rc = dalloc(ctx, &d.pin, n)) ||
+      (rc = dalloc(ctx, &d.gid, n)) || (rc = dalloc(ctx, &d.gids, (size_t)std::max(d.k, 1))) ||
+      (rc = dalloc(ctx, &d.e_after, (size_t)std::max(d.k, 1) * d.nw32)) ||
+      (rc = dalloc(ctx, &d.e_before, (size_t)std::max(d.k, 1) * d.nw32))) {
+    sip_kernel_destroy(k);
+    return rc;
+  }
+  if ((rc = h2d(ctx, d.meta, meta.data(), n)) || (rc = h2d(ctx, d.klass, t->klass, n)) ||
+      (rc = h2d(ctx, d.reads, t->reads, n * d.words)) ||
+      (rc = h2d(ctx, d.writes, t->writes, n * d.words)) ||
+      (rc = h2d(ctx, d.refs, t->refs, n * SIP_MAX_REFS)) || (rc = h2d(ctx, d.nrefs, t->nrefs, n)) ||
+      (rc = h2d(ctx, d.cut, t->cut, n + 1)) || (rc = h2d(ctx, d.pin, pin.data(), n)) ||
+      (rc = h2d(ctx, d.gid, gid.data(), n)) || (rc = h2d(ctx, d.gids, gids.data(), gids.size()))) {
+    sip_kernel_destroy(k);
+    return rc;
+  }
+  if (d.k > 0) {
+    dim3 grid((d.nw32 * 32 + 127) / 128, d.k);
+    legality_build_kernel<<<grid, 128, 0, ctx->stream>>>(d);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      sip_kernel_destroy(k);
+      return fail(ctx, SIP_E_CUDA, std::string("legality_build: ") + cudaGetErrorString(e));
+    }
+  }
+  // baseline scoreboard total of the identity schedule
+  std::vector<uint16_t> ident(n);
+  for (size_t i = 0; i < n; ++i) ident[i] = (uint16_t)i;
+  int64_t total = 0;
+  *out = k;
+  rc = sip_simulate(k, ident.data(), 1, &total, nullptr, nullptr);
+  if (rc != SIP_OK) {
+    sip_kernel_destroy(k);
+    *out = nullptr;
+    return rc;
+  }
+  k->baseline = total;
+  return SIP_OK;
+}
+
+int sip_kernel_destroy(sip_kernel* k) {
+  if (!k) return SIP_OK;
+  KernelDev& d = k->d;
+  void* ptrs[] = {d.meta, d.klass, d.reads, d.writes, d.refs, d.nrefs, d.cut,
+                  d.pin,  d.gid,   d.gids,  d.e_after, d.e_before};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete k;
+  return SIP_OK;
+}
+
+int sip_kernel_candidates(sip_kernel* k, int32_t* count) {
+  if (!k || !count) return SIP_E_ARG;
+  *count = k->d.k;
+  return SIP_OK;
+}
+
+int sip_legality_rows(sip_kernel* k, uint32_t* after, uint32_t* before) {
+  if (!k) return SIP_E_ARG;
+  sip_ctx* ctx = k->ctx;
+  size_t words = (size_t)k->d.k * k->d.nw32;
+  if (after) TRY(d2h(ctx, after, k->d.e_after, words));
+  if (before) TRY(d2h(ctx, before, k->d.e_before, words));
+  SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return SIP_OK;
+}
+
+int sip_legality_query(sip_kernel* k, const uint16_t* sched, const int32_t* lo, int32_t nq,
+                       int32_t hw_safe, int32_t min_fixed_distance, uint8_t* legal) {
+  if (!k || !sched || !lo || !legal || nq < 0) return SIP_E_ARG;
+  if (nq == 0) return SIP_OK;
+  sip_ctx* ctx = k->ctx;
+  uint16_t* ds = nullptr;
+  int32_t* dl = nullptr;
+  uint8_t* dg = nullptr;
+  size_t n = k->d.n;
+  int rc = SIP_OK;
+  if ((rc = dalloc(ctx, &ds, n * nq)) || (rc = dalloc(ctx, &dl, nq)) || (rc = dalloc(ctx, &dg, nq)))
+    goto done;
+  if ((rc = h2d(ctx, ds, sched, n * nq)) || (rc = h2d(ctx, dl, lo, nq))) goto done;
+  legality_query_kernel<<<(nq + 127) / 128, 128, 0, ctx->stream>>>(k->d, ds, dl, nq, hw_safe,
+                                                                   min_fixed_distance, dg);
+  if (cudaGetLastError() != cudaSuccess) {
+    rc = fail(ctx, SIP_E_CUDA, "legality_query launch failed");
+    goto done;
+  }
+  if ((rc = d2h(ctx, legal, dg, nq))) goto done;
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+    rc = fail(ctx, SIP_E_CUDA, "legality_query sync failed");
+done:
+  cudaFree(ds);
+  cudaFree(dl);
+  cudaFree(dg);
+  return rc;
+}
+
+int sip_simulate(sip_kernel* k, const uint16_t* scheds, int32_t count, int64_t* totals,
+                 int32_t* waited, int8_t* binding) {
+  if (!k || !scheds || !totals || count < 0) return SIP_E_ARG;
+  if ((waited == nullptr) != (binding == nullptr)) return SIP_E_ARG;
+  if (count == 0) return SIP_OK;
+  sip_ctx* ctx = k->ctx;
+  size_t n = k->d.n;
+  uint16_t* ds = nullptr;
+  int64_t* dt = nullptr;
+  int32_t* dw = nullptr;
+  int8_t* db = nullptr;
+  int rc = SIP_OK;
+  if ((rc = dalloc(ctx, &ds, n * count)) || (rc = dalloc(ctx, &dt, count))) goto done;
+  if (waited && ((rc = dalloc(ctx, &dw, n * count)) || (rc = dalloc(ctx, &db, n * count)))) goto done;
+  if ((rc = h2d(ctx, ds, scheds, n * count))) goto done;
+  simulate_kernel<<<(count + 127) / 128, 128, 0, ctx->stream>>>(k->d, ds, count, dt, dw, db);
+  if (cudaGetLastError() != cudaSuccess) {
+    rc = fail(ctx, SIP_E_CUDA, "simulate launch failed");
+    goto done;
+  }
+  if ((rc = d2h(ctx, totals, dt, count))) goto done;
+  if (waited && ((rc = d2h(ctx, waited, dw, n * count)) || (rc = d2h(ctx, binding, db, n * count))))
+    goto done;
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+    rc = fail(ctx, SIP_E_CUDA, "simulate sync failed");
+done:
+  cudaFree(ds);
+  cudaFree(dt);
+  if (dw) cudaFree(dw);
+  if (db) cudaFree(db);
+  return rc;
+}
+
+int sip_anneal(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds, int32_t chains,
+               sip_record* history, uint16_t* best, uint16_t* current, sip_chain_summary* summary) {
+  if (!k || !cfg || !seeds || chains < 1 || cfg->budget < 0) return SIP_E_ARG;
+  sip_ctx* ctx = k->ctx;
+  if (k->d.k == 0) return fail(ctx, SIP_E_NOCAND, "no global-memory instructions to move");
+  sip_chains o;
+  o.k = k;
+  int rc = chains_alloc(ctx, k, cfg, chains, seeds, &o);
+  uint32_t* d_base = nullptr;
+  if (rc == SIP_OK) rc = dalloc(ctx, &d_base, MT_N);
+  if (rc == SIP_OK) rc = h2d(ctx, d_base, mt_base_host().data(), MT_N);
+  if (rc == SIP_OK) {
+    size_t sm = smem_need(k->d);
+    int use_smem = sm <= kSmemCap;
+    if (use_smem) rc = configure_smem(ctx, (const void*)anneal_fused_kernel, sm);
+    if (rc == SIP_OK) {
+      anneal_fused_kernel<<<(chains + 127) / 128, 128, use_smem ? sm : 0, ctx->stream>>>(
+          k->d, o.s, d_base, use_smem, (double)k->baseline);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) rc = fail(ctx, SIP_E_CUDA, std::string("anneal: ") + cudaGetErrorString(e));
+    }
+  }
+  if (rc == SIP_OK) rc = chains_fetch(&o, history, best, current, summary);
+  if (d_base) cudaFree(d_base);
+  chains_free(&o);
+  return rc;
+}
+
+int sip_chains_create(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds,
+                      const double* t0, int32_t chains, sip_chains** out) {
+  if (!k || !cfg || !seeds || !t0 || chains < 1 || !out) return SIP_E_ARG;
+  sip_ctx* ctx = k->ctx;
+  if (k->d.k == 0) return fail(ctx, SIP_E_NOCAND, "no global-memory instructions to move");
+  auto* o = new sip_chains();
+  o->k = k;
+  int rc = chains_alloc(ctx, k, cfg, chains, seeds, o);
+  uint32_t* d_base = nullptr;
+  double* d_t0 = nullptr;
+  if (rc == SIP_OK) rc = dalloc(ctx, &d_base, MT_N);
+  if (rc == SIP_OK) rc = dalloc(ctx, &d_t0, chains);
+  if (rc == SIP_OK) rc = dalloc(ctx, &o->d_tcurr, chains);
+  if (rc == SIP_OK) rc = dalloc(ctx, &o->d_status, chains);
+  if (rc == SIP_OK) rc = dalloc(ctx, &o->d_lo, chains);
+  if (rc == SIP_OK) rc = dalloc(ctx, &o->s.cand_out, (size_t)chains * k->d.n);
+  if (rc == SIP_OK) rc = h2d(ctx, d_base, mt_base_host().data(), MT_N);
+  if (rc == SIP_OK) rc = h2d(ctx, d_t0, t0, chains);
+  if (rc == SIP_OK) {
+    chains_init_kernel<<<(chains + 127) / 128, 128, 0, ctx->stream>>>(k->d, o->s, d_base, d_t0);
+    if (cudaGetLastError() != cudaSuccess) rc = fail(ctx, SIP_E_CUDA, "chains_init launch failed");
+  }
+  if (rc == SIP_OK && cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+    rc = fail(ctx, SIP_E_CUDA, "chains_init failed");
+  if (d_base) cudaFree(d_base);
+  if (d_t0) cudaFree(d_t0);
+  if (rc != SIP_OK) {
+    chains_free(o);
+    delete o;
+    return rc;
+  }
+  *out = o;
+  return SIP_OK;
+}
+
+int sip_chains_propose(sip_chains* o, int32_t* lo, uint16_t* sched) {
+  if (!o || !lo) return SIP_E_ARG;
+  sip_kernel* k = o->k;
+  sip_ctx* ctx = k->ctx;
+  size_t sm = smem_need(k->d);
+  int use_smem = sm <= kSmemCap;
+  if (use_smem) TRY(configure_smem(ctx, (const void*)chains_propose_kernel, sm));
+  int C = o->s.C;
+  chains_propose_kernel<<<(C + 127) / 128, 128, use_smem ? sm : 0, ctx->stream>>>(k->d, o->s,
+                                                                                 use_smem, o->d_lo);
+  SIP_CHECK_LAUNCH(ctx);
+  TRY(d2h(ctx, lo, o->d_lo, C));
+  if (sched) TRY(d2h(ctx, sched, o->s.cand_out, (size_t)C * k->d.n));
+  SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return SIP_OK;
+}
+
+int sip_chains_resolve(sip_chains* o, const double* t_curr, const uint8_t* status) {
+  if (!o || !t_curr || !status) return SIP_E_ARG;
+  sip_ctx* ctx = o->k->ctx;
+  int C = o->s.C;
+  TRY(h2d(ctx, o->d_tcurr, t_curr, C));
+  TRY(h2d(ctx, o->d_status, status, C));
+  chains_resolve_kernel<<<(C + 127) / 128, 128, 0, ctx->stream>>>(o->k->d, o->s, o->d_tcurr,
+                                                                  o->d_status);
+  SIP_CHECK_LAUNCH(ctx);
+  SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return SIP_OK;
+}
+
+int sip_chains_adopt(sip_chains* o, const uint16_t* sched, double energy, double time) {
+  (void)time;
+  if (!o || !sched) return SIP_E_ARG;
+  sip_ctx* ctx = o->k->ctx;
+  if (!o->d_adopt) TRY(dalloc(ctx, &o->d_adopt, o->s.n));
+  TRY(h2d(ctx, o->d_adopt, sched, o->s.n));
+  chains_adopt_kernel<<<(o->s.C + 127) / 128, 128, 0, ctx->stream>>>(o->k->d, o->s, o->d_adopt,
+                                                                    energy);
+  SIP_CHECK_LAUNCH(ctx);
+  SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return SIP_OK;
+}
+
+int sip_chains_result(sip_chains* o, sip_record* history, uint16_t* best, uint16_t* current,
+                      sip_chain_summary* summary) {
+  if (!o) return SIP_E_ARG;
+  return chains_fetch(o, history, best, current, summary);
+}
+
+int sip_chains_destroy(sip_chains* o) {
+  if (!o) return SIP_OK;
+  chains_free(o);
+  delete o;
+  return SIP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,114 @@
+"""Multi-chain search (reference ``driver.py:52-116``) with batched chains.
+
+Chains ``seed .. seed+C-1`` are independent (``driver.py:73-79``).  The
+reference runs them one after another; here
+
+* simulator energy: all C chains run in ONE device launch (``sip_anneal``);
+* hardware energy (``B200Backend``): all C chains advance together in step
+  mode, the device proposing, the evaluator pricing one candidate per chain
+  per round;
+* any other backend (possibly stateful, e.g. a counting or failing test
+  double): chains run sequentially in step mode, exactly in the reference's
+  call order.
+
+Ranking, verification and the store follow the reference unchanged:
+champions are verified on the full plan, passing chains are ranked by
+``(best_time, seed)``.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, replace
+
+from .anneal import AnnealConfig, AnnealState, anneal_batch_sim, anneal_steps, uses_device_energy
+from .ir import Kernel
+from .perturb import candidates
+from .sasstext import serialize_kernel
+from .store import ResultStore, input_hash
+
+
+@dataclass
+class ChainOutcome:
+    seed: int
+    state: AnnealState
+    verdict: object | None
+
+    @property
+    def passed(self) -> bool:
+        return True if self.verdict is None else self.verdict.ok
+
+
+@dataclass
+class SearchReport:
+    kernel: Kernel
+    input_digest: str
+    baseline: float
+    unit: str
+    chains: list
+    best: ChainOutcome | None
+    candidate_count: int = 0
+
+    @property
+    def best_time(self) -> float | None:
+        return None if self.best is None else self.best.state.best_time
+
+    @property
+    def improvement_pct(self) -> float | None:
+        if self.best is None or self.baseline <= 0:
+            return None
+        return (self.baseline - self.best.state.best_time) / self.baseline * 100.0
+
+
+def _tester(kernel, plan, cfg):
+    if plan is None or cfg.tests_per_step <= 0:
+        return None
+    from .difftest import run_tests
+
+    step_plan = replace(plan, samples=cfg.tests_per_step)
+    return lambda cand: run_tests(kernel, cand, step_plan, fail_fast=True).ok
+
+
+def run_states(kernel: Kernel, backend, cfg: AnnealConfig, chains: int, tester=None,
+               tables=None, on_epoch=None) -> list:
+    seeds = [cfg.seed + c for c in range(chains)]
+    if tester is None and uses_device_energy(backend):
+        return anneal_batch_sim(kernel, backend.machine, cfg, seeds, tables=tables)
+    if getattr(backend, "batched_chains", False):
+        return anneal_steps(kernel, backend, cfg, seeds, tester=tester, tables=tables,
+                            on_epoch=on_epoch)
+    states = []
+    for s in seeds:
+        states += anneal_steps(kernel, backend, replace(cfg, seed=s), [s], tester=tester,
+                               tables=tables)
+    return states
+
+
+def run_search(kernel: Kernel, backend, anneal_cfg: AnnealConfig, *, chains: int = 1,
+               plan=None, store: ResultStore | None = None, on_epoch=None) -> SearchReport:
+    if chains < 1:
+        raise ValueError("chains must be >= 1")
+    digest = input_hash(serialize_kernel(kernel))
+    states = run_states(kernel, backend, anneal_cfg, chains, _tester(kernel, plan, anneal_cfg),
+                        on_epoch=on_epoch)
+    outcomes = []
+    for c, st in enumerate(states):
+        verdict = None
+        if plan is not None:
+            from .difftest import run_tests
+
+            verdict = run_tests(kernel, st.best, plan)
+        outcomes.append(ChainOutcome(anneal_cfg.seed + c, st, verdict))
+    baseline = states[-1].baseline if states else 0.0
+    unit = states[-1].unit if states else getattr(backend, "unit", "")
+    ranked = sorted((o for o in outcomes if o.passed), key=lambda o: (o.state.best_time, o.seed))
+    best = ranked[0] if ranked else None
+
+    if store is not None:
+        entries = []
+        for o in outcomes:
+            vd = o.verdict.to_dict() if o.verdict is not None else {"skipped": True}
+            store.write_chain(digest, o.seed, serialize_kernel(o.state.best), o.state.history_jsonl(), vd)
+            entries.append({"seed": o.seed, "time": o.state.best_time, "passed": o.passed,
+                            "iterations": o.state.iterations})
+        store.update_manifest(digest, baseline=baseline, unit=unit, entries=entries)
+
+    return SearchReport(kernel, digest, baseline, unit, outcomes, best, len(candidates(kernel)))

@@ -1,0 +1,114 @@
+"""CUDA search engine (G1 legality, G2 annealing, scoreboard) vs reference goldens
+and vs the CPU oracle.  Bit-exact: histories compared as JSONL bytes."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import golden, listing_names
+from golden_configs import CONFIGS
+from oracle import oracle
+from paper_2403_16863_b200 import (AnnealConfig, SimulatorBackend, anneal, parse_kernel, run_search,
+                                   simulate)
+from paper_2403_16863_b200.anneal import anneal_batch_sim
+from paper_2403_16863_b200.engine import get_context
+from paper_2403_16863_b200.machine import MachineConfig
+from paper_2403_16863_b200.tables import KernelTables
+
+pytestmark = pytest.mark.gpu
+
+ANNEAL_NAMES = listing_names(lambda r: "anneal" in r)
+SIM_NAMES = listing_names(lambda r: "sim" in r)
+WALK_NAMES = listing_names(lambda r: r["walks"])
+
+
+def setup(name):
+    rec = golden()["listings"][name]
+    k = parse_kernel(rec["text"], name=name)
+    t = KernelTables.build(k, MachineConfig())
+    return rec, k, t, get_context().kernel(t)
+
+
+@pytest.mark.parametrize("name", SIM_NAMES)
+def test_simulate_report_matches_reference(name):
+    rec, k, t, dk = setup(name)
+    assert simulate(k).to_json() == rec["sim"]["json"]
+
+
+@pytest.mark.parametrize("name", WALK_NAMES)
+def test_legality_matches_reference_walks(name):
+    rec, k, t, dk = setup(name)
+    n = t.n
+    for w in rec["walks"]:
+        los = np.arange(n - 1, dtype=np.int32)
+        scheds = np.tile(np.asarray(w["perm"], dtype=np.uint16), (n - 1, 1))
+        assert dk.legality(scheds, los).tolist() == w["legal"]
+
+
+@pytest.mark.parametrize("name", ANNEAL_NAMES)
+def test_anneal_histories_byte_identical(name):
+    rec, k, t, dk = setup(name)
+    for cname, runs in rec["anneal"].items():
+        cfg = AnnealConfig(**CONFIGS[cname])
+        seeds = [int(s) for s in runs]
+        states = anneal_batch_sim(k, MachineConfig(), cfg, seeds, tables=t)
+        for seed, st in zip(seeds, states):
+            want = runs[str(seed)]
+            jsonl = st.history_jsonl()
+            if "jsonl" in want:
+                assert jsonl == want["jsonl"], (cname, seed)
+            assert hashlib.sha256(jsonl.encode()).hexdigest() == want["sha256"], (cname, seed)
+            assert st.best_perm.tolist() == want["best"]
+            assert st.best_energy == want["best_energy"]
+            assert st.current_energy == want["current_energy"]
+            assert st.baseline == want["baseline"]
+            assert st.ambiguous == 0
+
+
+def test_public_anneal_api_single_chain():
+    rec, k, t, dk = setup("hide")
+    st = anneal(k, SimulatorBackend(), AnnealConfig(seed=0))
+    assert st.baseline == 436.0 and st.best_time == 404.0 and st.iterations == 95
+    assert st.history_jsonl() == rec["anneal"]["default"]["0"]["jsonl"]
+
+
+class _PythonPricedSim(SimulatorBackend):
+    """Same energy as SimulatorBackend but priced through measure() -> step mode."""
+
+    def measure(self, kernel, reps=1):
+        return super().measure(kernel, reps)
+
+
+@pytest.mark.parametrize("name", ["copy_stage_a", "pipeline", "base_detect", "random_program_2"])
+def test_step_mode_matches_reference(name):
+    rec, k, t, dk = setup(name)
+    for seed in (0, 1):
+        st = anneal(k, _PythonPricedSim(), AnnealConfig(seed=seed))
+        want = rec["anneal"]["default"][str(seed)]
+        assert hashlib.sha256(st.history_jsonl().encode()).hexdigest() == want["sha256"]
+
+
+@pytest.mark.parametrize("name", ["synthetic_mix_0", "synthetic_mix_1", "random_program_0", "corridor"])
+@pytest.mark.parametrize("cname", ["default", "long"])
+def test_many_chains_vs_oracle(name, cname):
+    """Hundreds of seeds beyond the goldens: device records == oracle records."""
+    rec, k, t, dk = setup(name)
+    cfg = AnnealConfig(**CONFIGS[cname])
+    temps = cfg.temperatures()
+    seeds = np.arange(1000, 1000 + (256 if cname == "default" else 64), dtype=np.int64)
+    hist, best, cur, summ = dk.anneal(seeds, temps)
+    ol = oracle.OracleListing(t)
+    for c, s in enumerate(seeds):
+        oh, ob, oc, os_ = ol.anneal(int(s), temps)
+        assert np.array_equal(hist[c], oh), (name, int(s))
+        assert np.array_equal(best[c], ob) and np.array_equal(cur[c], oc)
+        assert summ["best_energy"][c] == os_["best_energy"]
+    assert int(summ["ambiguous"].sum()) == 0
+
+
+def test_run_search_batched_ranking():
+    rec, k, t, dk = setup("hide")
+    rep = run_search(k, SimulatorBackend(), AnnealConfig(seed=0), chains=8)
+    assert [o.seed for o in rep.chains] == list(range(8))
+    assert rep.best_time == 404.0 and rep.best.seed == 0
+    assert rep.baseline == 436.0

@@ -1,0 +1,74 @@
+"""Host frontend vs the reference: parse/serialize, classes, cuts, register and
+memory facts -- checked listing by listing against goldens produced by the
+reference itself (tests/golden/make_golden.py)."""
+import pytest
+
+from conftest import golden, listing_names
+from paper_2403_16863_b200 import (ControlCode, ParseError, candidates, classify, mem_refs,
+                                   parse_control, parse_kernel, reads_writes, serialize_kernel)
+from paper_2403_16863_b200.ir import InstrClass
+from paper_2403_16863_b200.sasstext import normalize_newlines
+
+NAMES = listing_names()
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_round_trip(name):
+    rec = golden()["listings"][name]
+    k = parse_kernel(rec["text"], name=name)
+    assert len(k.schedule) == rec["n"]
+    assert (serialize_kernel(k) == normalize_newlines(rec["text"])) == rec["serialize_ok"]
+    assert rec["serialize_ok"]
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_structure_matches_reference(name):
+    rec = golden()["listings"][name]
+    k = parse_kernel(rec["text"], name=name)
+    assert list(k.block_boundaries) == rec["cuts"]
+    assert list(candidates(k).positions) == rec["cands"]
+    assert [ins.klass.value for ins in k.schedule] == rec["classes"]
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_register_sets_match_reference(name):
+    rec = golden()["listings"][name]
+    k = parse_kernel(rec["text"], name=name)
+    for i, ins in enumerate(k.schedule):
+        r, w = reads_writes(ins)
+        assert [sorted(r), sorted(w)] == rec["rw"][i], (i, ins.source_text)
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_memory_refs_match_reference(name):
+    rec = golden()["listings"][name]
+    k = parse_kernel(rec["text"], name=name)
+    for i, ins in enumerate(k.schedule):
+        got = [[m.space, m.base, m.offset, m.size, int(m.write)] for m in mem_refs(ins)]
+        assert got == rec["refs"][i], (i, ins.source_text)
+
+
+def test_control_text_round_trip():
+    for text in ("[B------:R-:W-:-:S01]", "[B0-2--5:R3:W1:Y:S15]", "B-1----:R-:W0:-:S00"):
+        c = parse_control(text)
+        assert c.to_text() == (text if text.startswith("[") else f"[{text}]")
+
+
+@pytest.mark.parametrize("bad", ["[B------:R-:W-:-:S16]", "[B1-----:R-:W-:-:S01]",
+                                 "[B------:R6:W-:-:S01]", "[B------]"])
+def test_control_rejects_bad_fields(bad):
+    with pytest.raises(ValueError):
+        parse_control(bad)
+
+
+def test_parse_error_on_bad_control():
+    with pytest.raises(ParseError):
+        parse_kernel("[B------:R-:W-:-:S99] MOV R0, RZ ;\n")
+
+
+def test_classify_table():
+    assert classify("LDG.E.128") is InstrClass.GLOBAL_LOAD
+    assert classify("ldgsts.e.bypass.128") is InstrClass.GLOBAL_ASYNC_COPY
+    assert classify("UTMALDG.2D") is InstrClass.OTHER  # K6: TMA is OTHER under reference rules
+    assert classify("BAR.SYNC") is InstrClass.BARRIER
+    assert ControlCode().to_text() == "[B------:R-:W-:-:S01]"
