@@ -60,7 +60,7 @@ class AnnealConfig:
     tests_per_step: int = 0
     unsafe_moves: bool = False
     hw_safe: bool = False          # extension; False reproduces the reference
-    min_fixed_distance: int = 12   # hw_safe: issue distance a fixed-latency RAW pair keeps
+    min_fixed_distance: int = 8    # hw_safe: issue distance a fixed-latency RAW pair keeps
 
     def __post_init__(self) -> None:
         if self.t_min <= 0 or self.t_max <= 0:
@@ -270,4 +270,8 @@ def anneal(kernel: Kernel, backend, config: AnnealConfig | None = None, *,
     cfg = config or AnnealConfig()
     if uses_device_energy(backend) and tester is None:
         return anneal_batch_sim(kernel, backend.machine, cfg, [cfg.seed])[0]
-    return anneal_steps(kernel, backend, cfg, [cfg.seed], tester=tester)[0]
+    from .driver import hardware_config
+
+    cfg = hardware_config(backend, cfg)
+    tables = backend.tables_for(kernel) if hasattr(backend, "tables_for") else None
+    return anneal_steps(kernel, backend, cfg, [cfg.seed], tester=tester, tables=tables)[0]

@@ -22,7 +22,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 
 LIB_SOURCES = ["context.cu", "engine.cu", "evaluator.cu", "verify.cu", "targets_launch.cu"]
-CUBINS = {"gemm_lrelu": "gemm_lrelu.cu", "attn_fwd": "attn_fwd.cu"}
+CUBINS = {"gemm_lrelu": "gemm_lrelu.cu", "attn_fwd": "attn_fwd.cu", "canary": "canary.cu"}
 
 
 def _run(cmd, cwd=None) -> None:

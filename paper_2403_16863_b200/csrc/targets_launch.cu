@@ -1,0 +1,107 @@
+// targets_launch.cu -- launch descriptors (grid, smem, packed arguments with TMA
+// tensor maps) for the shipped tuning-target cubins (targets/*.cu).  The
+// evaluator launches whatever permutation of those cubins the search proposes
+// with exactly these arguments.
+#include <cstring>
+
+#include "common.h"
+
+namespace {
+
+constexpr uint32_t kGemmOffsets[8] = {0, 128, 256, 264, 268, 272, 276, 280};
+constexpr uint32_t kGemmParamBytes = 284;
+constexpr uint32_t kAttnOffsets[9] = {0, 128, 256, 384, 392, 396, 400, 404, 408};
+constexpr uint32_t kAttnParamBytes = 412;
+
+int encode(sip_ctx* ctx, CUtensorMap* map, const void* base, int rank, const cuuint64_t* dims,
+           const cuuint64_t* strides_bytes, const cuuint32_t* box) {
+  cuuint32_t elem[5] = {1, 1, 1, 1, 1};
+  CUresult r = ctx->cuTensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, rank, const_cast<void*>(base),
+                                           dims, strides_bytes, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return sip::fail(ctx, SIP_E_ARG, "cuTensorMapEncodeTiled failed");
+  return SIP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sip_target_gemm_launch(sip_ctx* ctx, const void* A, const void* B, void* C, int32_t M, int32_t N,
+                           int32_t K, int32_t L, float slope, sip_launch* launch, void* params,
+                           uint32_t params_cap) {
+  if (!ctx || !A || !B || !C || !launch || !params || params_cap < kGemmParamBytes) return SIP_E_ARG;
+  if (M <= 0 || N <= 0 || K <= 0 || L <= 0 || M % 128 || N % 256 || K % 64)
+    return sip::fail(ctx, SIP_E_ARG, "gemm target needs M%128==0, N%256==0, K%64==0");
+  uint8_t* p = static_cast<uint8_t*>(params);
+  std::memset(p, 0, kGemmParamBytes);
+  cuuint64_t da[3] = {(cuuint64_t)K, (cuuint64_t)M, (cuuint64_t)L};
+  cuuint64_t sa[2] = {(cuuint64_t)K * 2, (cuuint64_t)M * K * 2};
+  cuuint32_t ba[3] = {64, 128, 1};
+  cuuint64_t db[3] = {(cuuint64_t)K, (cuuint64_t)N, (cuuint64_t)L};
+  cuuint64_t sb[2] = {(cuuint64_t)K * 2, (cuuint64_t)N * K * 2};
+  cuuint32_t bb[3] = {64, 256, 1};
+  int rc = encode(ctx, reinterpret_cast<CUtensorMap*>(p), A, 3, da, sa, ba);
+  if (rc == SIP_OK) rc = encode(ctx, reinterpret_cast<CUtensorMap*>(p + 128), B, 3, db, sb, bb);
+  if (rc != SIP_OK) return rc;
+  std::memcpy(p + 256, &C, 8);
+  std::memcpy(p + 264, &M, 4);
+  std::memcpy(p + 268, &N, 4);
+  std::memcpy(p + 272, &K, 4);
+  std::memcpy(p + 276, &L, 4);
+  std::memcpy(p + 280, &slope, 4);
+  long tiles = (long)(M / 128) * (N / 256) * L;
+  std::memset(launch, 0, sizeof *launch);
+  launch->grid[0] = (uint32_t)(tiles < ctx->sm_count ? tiles : ctx->sm_count);
+  launch->grid[1] = launch->grid[2] = 1;
+  launch->block[0] = 192;
+  launch->block[1] = launch->block[2] = 1;
+  launch->cluster[0] = launch->cluster[1] = launch->cluster[2] = 1;
+  launch->smem_bytes = 4 * (128 * 64 * 2 + 256 * 64 * 2) + 1024 + 256;
+  launch->params = params;
+  launch->param_offsets = kGemmOffsets;
+  launch->nparams = 8;
+  launch->params_size = kGemmParamBytes;
+  return SIP_OK;
+}
+
+int sip_target_attn_launch(sip_ctx* ctx, const void* Q, const void* K, const void* V, void* O, int32_t B,
+                           int32_t H, int32_t S, int32_t D, float scale, sip_launch* launch, void* params,
+                           uint32_t params_cap) {
+  if (!ctx || !Q || !K || !V || !O || !launch || !params || params_cap < kAttnParamBytes) return SIP_E_ARG;
+  if (B <= 0 || H <= 0 || S <= 0 || D != 128 || S % 128)
+    return sip::fail(ctx, SIP_E_ARG, "attention target needs D == 128 and S % 128 == 0");
+  uint8_t* p = static_cast<uint8_t*>(params);
+  std::memset(p, 0, kAttnParamBytes);
+  // [B*H][S][D] viewed as 4-D (64-col half, S, 2 halves of D, B*H) for SWIZZLE_128B boxes of 64 x rows
+  cuuint64_t dims[4] = {64, (cuuint64_t)S, 2, (cuuint64_t)B * H};
+  cuuint64_t strides[3] = {(cuuint64_t)D * 2, 64 * 2, (cuuint64_t)S * D * 2};
+  cuuint32_t box_q[4] = {64, 128, 2, 1};
+  cuuint32_t box_kv[4] = {64, 128, 2, 1};
+  int rc = encode(ctx, reinterpret_cast<CUtensorMap*>(p), Q, 4, dims, strides, box_q);
+  if (rc == SIP_OK) rc = encode(ctx, reinterpret_cast<CUtensorMap*>(p + 128), K, 4, dims, strides, box_kv);
+  if (rc == SIP_OK) rc = encode(ctx, reinterpret_cast<CUtensorMap*>(p + 256), V, 4, dims, strides, box_kv);
+  if (rc != SIP_OK) return rc;
+  std::memcpy(p + 384, &O, 8);
+  std::memcpy(p + 392, &B, 4);
+  std::memcpy(p + 396, &H, 4);
+  std::memcpy(p + 400, &S, 4);
+  std::memcpy(p + 404, &D, 4);
+  std::memcpy(p + 408, &scale, 4);
+  std::memset(launch, 0, sizeof *launch);
+  launch->grid[0] = (uint32_t)(S / 128);
+  launch->grid[1] = (uint32_t)(B * H);
+  launch->grid[2] = 1;
+  launch->block[0] = 256;
+  launch->block[1] = launch->block[2] = 1;
+  launch->cluster[0] = launch->cluster[1] = launch->cluster[2] = 1;
+  launch->smem_bytes = 0;  // set by the attention target once it lands
+  launch->params = params;
+  launch->param_offsets = kAttnOffsets;
+  launch->nparams = 9;
+  launch->params_size = kAttnParamBytes;
+  return SIP_OK;
+}
+
+}  // extern "C"

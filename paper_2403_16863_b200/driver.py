@@ -67,8 +67,20 @@ def _tester(kernel, plan, cfg):
     return lambda cand: run_tests(kernel, cand, step_plan, fail_fast=True).ok
 
 
+def hardware_config(backend, cfg: AnnealConfig) -> AnnealConfig:
+    """Candidates that execute on the GPU must respect stall distances, reuse
+    bits and pinned offsets; the extension is forced on."""
+    if getattr(backend, "hardware", False):
+        return replace(cfg, hw_safe=True,
+                       min_fixed_distance=max(cfg.min_fixed_distance, backend.min_fixed))
+    return cfg
+
+
 def run_states(kernel: Kernel, backend, cfg: AnnealConfig, chains: int, tester=None,
                tables=None, on_epoch=None) -> list:
+    cfg = hardware_config(backend, cfg)
+    if tables is None and hasattr(backend, "tables_for"):
+        tables = backend.tables_for(kernel)
     seeds = [cfg.seed + c for c in range(chains)]
     if tester is None and uses_device_energy(backend):
         return anneal_batch_sim(kernel, backend.machine, cfg, seeds, tables=tables)

@@ -1,0 +1,109 @@
+"""Hardware cost backend (G4): real B200 timing of permuted sm_100a cubins.
+
+``B200Backend.measure(kernel, reps)`` keeps the reference contract
+(``backends.py:32-39``): the kernel is a (permuted) listing produced by the
+cubin frontend; its schedule is turned into a word permutation, the patched
+cubin is loaded with ``cuModuleLoadData`` and ``warmup + reps`` launches are
+replayed from one CUDA graph with CUDA events around each timed launch
+(``sip_measure``).  The value is the median in milliseconds, like the
+reference's external protocol (``{"time_ms": x}``, backends.py:25).  Any load
+or launch failure raises ``MeasurementFailed``.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from .backends import BackendDescriptor, CostSample, MeasurementFailed
+from .cubin import Listing, Module, render_listing, schedule_perm
+from .engine import SIP_E_MEASURE, EngineError, c_dblp, c_u16p, get_context
+from .ir import Kernel
+from .targets import make_target
+
+FIXED_LAT_HEAVY = ("HMMA", "IMMA", "DMMA", "BMMA", "HGMMA", "DFMA", "DADD", "DMUL")
+
+
+def min_fixed_distance(kernel: Kernel) -> int:
+    """Issue distance (cycles) a fixed-latency producer must keep to its consumer
+    in hw_safe mode: 8 covers the ALU/FMA/conversion pipes (latency 4-6 on
+    Blackwell); listings with legacy tensor or FP64 ops get 40."""
+    heavy = any(ins.base_mnemonic in FIXED_LAT_HEAVY for ins in kernel.schedule)
+    return 40 if heavy else 8
+
+
+class B200Backend:
+    unit = "ms"
+    batched_chains = True  # run_search advances all chains together (driver.py)
+    hardware = True        # candidates execute on the GPU: hw_safe legality is enforced
+
+    def __init__(self, target, listing: Listing | None = None, *, device: int = 0, warmup: int = 2,
+                 flush_l2: bool = True):
+        self.target = target
+        self.device = device
+        self.ctx = get_context(device)
+        cubin, func = target.cubin()
+        self.listing = listing or render_listing(cubin, func)
+        self.module = Module(cubin, func, ctx=self.ctx)
+        self.warmup = warmup
+        self.flush_l2 = flush_l2
+        self.launch, self._params = target.launch()
+        self.descriptor = BackendDescriptor(kind="b200", command=func, concurrency_safe=False)
+        self.calls = 0
+        self.kernel_ms = []  # every timed launch (ms), for roofline accounting
+
+    @classmethod
+    def for_target(cls, kind: str, device: int = 0, **kw):
+        tgt = make_target(kind, device=device, **kw).allocate()
+        return cls(tgt, device=device)
+
+    @property
+    def kernel(self) -> Kernel:
+        return self.listing.kernel
+
+    @property
+    def min_fixed(self) -> int:
+        return min_fixed_distance(self.listing.kernel)
+
+    def tables_for(self, kernel: Kernel):
+        """Device tables of `kernel` (a permutation of the listing) with the cubin's
+        reuse bits and pinned instructions attached to each identity."""
+        from .machine import MachineConfig
+        from .tables import KernelTables
+
+        ids = schedule_perm(kernel)
+        reuse = [self.listing.reuse[int(i)] for i in ids]
+        pinned = [p for p, i in enumerate(ids) if self.listing.pins[int(i)]]
+        return KernelTables.build(kernel, MachineConfig(), reuse=reuse, pinned=pinned)
+
+    def perm_of(self, kernel: Kernel) -> np.ndarray:
+        return schedule_perm(kernel)
+
+    def measure_perm(self, perm, reps: int = 5) -> CostSample:
+        perm = np.ascontiguousarray(perm, dtype=np.uint16)
+        med = ctypes.c_double()
+        raw = np.zeros(reps, dtype=np.float64)
+        lib = self.ctx.lib
+        rc = lib.sip_measure(self.module.handle, perm.ctypes.data_as(c_u16p), ctypes.byref(self.launch),
+                             self.warmup, reps, int(self.flush_l2), ctypes.byref(med),
+                             raw.ctypes.data_as(c_dblp))
+        self.calls += 1
+        if rc == SIP_E_MEASURE:
+            raise MeasurementFailed(lib.sip_last_error(self.ctx.handle).decode(errors="replace"))
+        self.ctx.check(rc)
+        self.kernel_ms.extend(raw.tolist())
+        return CostSample(med.value, self.unit, reps, tuple(raw.tolist()))
+
+    def measure(self, kernel: Kernel, reps: int = 5) -> CostSample:
+        if len(kernel.schedule) != self.listing.n:
+            raise MeasurementFailed("schedule does not match the loaded cubin")
+        return self.measure_perm(self.perm_of(kernel), reps)
+
+    def run_perm(self, perm) -> None:
+        perm = None if perm is None else np.ascontiguousarray(perm, dtype=np.uint16)
+        lib = self.ctx.lib
+        rc = lib.sip_run(self.module.handle, None if perm is None else perm.ctypes.data_as(c_u16p),
+                         ctypes.byref(self.launch))
+        if rc == SIP_E_MEASURE:
+            raise MeasurementFailed(lib.sip_last_error(self.ctx.handle).decode(errors="replace"))
+        self.ctx.check(rc)

@@ -1,0 +1,155 @@
+// gemm_lrelu.cu -- tuning target G7: C = LeakyReLU(A * B^T), fp16 in/out, fp32 accumulate.
+//
+// The paper's GEMM+LeakyReLU workload, written by hand for
+// sm_100a instead of Triton/A100:
+//   * persistent: one CTA per SM, static round-robin over 128x256 output tiles
+//     (batched over L independent problems, used by the verifier);
+//   * warp 0: TMA producer (SWIZZLE_128B, 4-stage 48 KB ring, mbarrier full/empty);
+//   * warp 1: TMEM allocator + single-thread tcgen05.mma issuer (M128 N256 K16),
+//     accumulating in one of two 256-column TMEM buffers;
+//   * warps 2-5: epilogue -- tcgen05.ld 32 columns at a time, LeakyReLU in fp32,
+//     pack to fp16, 16-byte st.global per thread; the second TMEM buffer lets
+//     the epilogue of tile i overlap the main loop of tile i+1.
+// The epilogue's STG instructions are the global-memory instructions SIP may move
+// under the reference's candidate rules.
+//
+// Requirements (checked by the host launcher): M % 128 == 0, N % 256 == 0,
+// K % 64 == 0; A is [L][M][K], B is [L][N][K], C is [L][M][N], all row-major.
+#include "sm100.cuh"
+
+namespace {
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int ACC_COLS = BN, TMEM_COLS = 2 * ACC_COLS;
+constexpr int NUM_THREADS = 192;
+constexpr uint32_t IDESC = sm100::idesc_f16(BM, BN);
+}  // namespace
+
+extern "C" __global__ void __launch_bounds__(NUM_THREADS, 1)
+gemm_lrelu_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               __half* __restrict__ C, int M, int N, int K, int L, float slope) {
+  using namespace sm100;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* acc_full = empty + STAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = warp_id();
+  const int lane = threadIdx.x & 31;
+  const int tiles_m = M / BM, tiles_n = N / BN, kblocks = K / BK;
+  const int tiles = tiles_m * tiles_n * L;
+
+  if (warp == 0 && elect_one()) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 4);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 1) tmem_alloc<TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        int l = t / (tiles_m * tiles_n), r = t % (tiles_m * tiles_n);
+        int m0 = (r / tiles_n) * BM, n0 = (r % tiles_n) * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], STAGE_BYTES);
+          tma_load_3d(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, m0, l);
+          tma_load_3d(sB + stage * B_BYTES, &tmB, &full[stage], kb * BK, n0, l);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    int stage = 0;
+    uint32_t phase = 0;
+    int local = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+      const int buf = local & 1;
+      const uint32_t use = local >> 1;
+      mbar_wait(&acc_empty[buf], (use & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem + buf * ACC_COLS;
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t a0 = smem_u32(sA + stage * A_BYTES), b0 = smem_u32(sB + stage * B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)
+            mma_f16(d_tmem, desc_sw128(a0 + kk * 32), desc_sw128(b0 + kk * 32), IDESC, (kb | kk) != 0);
+          mma_commit(&empty[stage]);
+          if (kb == kblocks - 1) mma_commit(&acc_full[buf]);
+        }
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue: warps 2..5 ----------------
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int row_in_tile = quarter * 32 + lane;
+    int local = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+      const int buf = local & 1;
+      const uint32_t use = local >> 1;
+      int l = t / (tiles_m * tiles_n), r = t % (tiles_m * tiles_n);
+      int m0 = (r / tiles_n) * BM, n0 = (r % tiles_n) * BN;
+      mbar_wait(&acc_full[buf], use & 1);
+      tc_fence_after();
+      __half* crow = C + ((size_t)l * M + m0 + row_in_tile) * (size_t)N + n0;
+      const uint32_t t_base = tmem + ((uint32_t)(quarter * 32) << 16) + buf * ACC_COLS;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(t_base + c * 32, v);
+        tmem_ld_wait();
+        uint32_t h[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          h[j] = pack_half2(leaky(__uint_as_float(v[2 * j]), slope), leaky(__uint_as_float(v[2 * j + 1]), slope));
+        __half* dst = crow + c * 32;
+        stg128(dst, h[0], h[1], h[2], h[3]);
+        stg128(dst + 8, h[4], h[5], h[6], h[7]);
+        stg128(dst + 16, h[8], h[9], h[10], h[11]);
+        stg128(dst + 24, h[12], h[13], h[14], h[15]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+    }
+  }
+
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<TMEM_COLS>(tmem);
+  }
+}
