@@ -93,6 +93,9 @@ typedef struct {
   double current_energy; /* AnnealState.current_energy                */
   int32_t best_iter;     /* iteration that produced best (-1 = none)  */
   int32_t ambiguous;     /* Metropolis draws within 4 ulp of exp()    */
+  int64_t replayed;      /* scoreboard steps executed (instrumentation) */
+  int32_t priced;        /* iterations whose candidate was priced        */
+  int32_t pad;
 } sip_chain_summary;
 
 /* ---- context -------------------------------------------------------- */
@@ -125,6 +128,13 @@ int sip_simulate(sip_kernel* k, const uint16_t* scheds, int32_t count, int64_t* 
 int sip_anneal(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds, int32_t chains,
                sip_record* history /* [chains*budget] */, uint16_t* best /* [chains*n] */,
                uint16_t* current /* [chains*n] */, sip_chain_summary* summary /* [chains] */);
+
+/* same, starting every chain from `start` (identity when NULL); `champion`
+ * (optional, [n]) receives the best schedule over all chains ranked by
+ * (best energy, seed) as driver.run_search ranks them (driver.py:81-85). */
+int sip_anneal_ex(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds, int32_t chains,
+                  const uint16_t* start, sip_record* history, uint16_t* best, uint16_t* current,
+                  sip_chain_summary* summary, uint16_t* champion, int32_t* champion_chain);
 
 /* ---- G2 step mode: external energy (any backend.measure) ------------- */
 int sip_chains_create(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds,

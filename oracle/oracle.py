@@ -20,7 +20,8 @@ LIB = HERE / "_build" / "libsip_oracle.so"
 RECORD_DTYPE = np.dtype([("time", "<f8"), ("lo", "<i4"), ("candidate", "<u2"),
                          ("direction", "u1"), ("status", "u1")])
 SUMMARY_DTYPE = np.dtype([("t0", "<f8"), ("best_energy", "<f8"), ("current_energy", "<f8"),
-                          ("best_iter", "<i4"), ("ambiguous", "<i4")])
+                          ("best_iter", "<i4"), ("ambiguous", "<i4"), ("replayed", "<i8"),
+                          ("priced", "<i4"), ("pad", "<i4")])
 REASONS = {2: "boundary", 3: "dependency", 4: "test-failure", 5: "measurement", 6: "hw-safety"}
 
 _u16 = ctypes.POINTER(ctypes.c_uint16)

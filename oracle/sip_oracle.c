@@ -469,6 +469,10 @@ int oracle_anneal(const sip_tables* t, const double* temps, int budget, int unsa
     summary->current_energy = e_x;
     summary->best_iter = best_iter;
     summary->ambiguous = 0;
+    summary->replayed = 0;
+    summary->priced = 0;
+    for (int it = 0; it < budget; it++) summary->priced += hist[it].status <= SIP_ST_PRICED;
+    summary->pad = 0;
   }
   free(x); free(cand); free(best); free(adj); free(cpos);
   return SIP_OK;

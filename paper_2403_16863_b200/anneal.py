@@ -131,12 +131,15 @@ def records_to_history(records, t0: float, temps) -> list:
 class AnnealState:
     """Search outcome; ``history`` is materialised lazily from device records."""
 
-    def __init__(self, best: Kernel, best_energy: float, current: Kernel, current_energy: float,
-                 baseline: float, unit: str, iterations: int, history=None, *, records=None,
-                 temps=None, best_perm=None, ambiguous: int = 0):
-        self.best = best
+    def __init__(self, best: Kernel | None, best_energy: float, current: Kernel | None,
+                 current_energy: float, baseline: float, unit: str, iterations: int, history=None,
+                 *, records=None, temps=None, best_perm=None, current_perm=None, base=None,
+                 ambiguous: int = 0):
+        self._best = best
+        self._current = current
+        self._base = base  # listing the permutations index into (kernels built on access)
+        self.current_perm = current_perm
         self.best_energy = best_energy
-        self.current = current
         self.current_energy = current_energy
         self.baseline = baseline
         self.unit = unit
@@ -146,6 +149,18 @@ class AnnealState:
         self._temps = temps
         self.best_perm = best_perm
         self.ambiguous = ambiguous
+
+    @property
+    def best(self) -> Kernel:
+        if self._best is None and self._base is not None and self.best_perm is not None:
+            self._best = _permuted(self._base, self.best_perm)
+        return self._best
+
+    @property
+    def current(self) -> Kernel:
+        if self._current is None and self._base is not None and self.current_perm is not None:
+            self._current = _permuted(self._base, self.current_perm)
+        return self._current
 
     @property
     def history(self) -> list:
@@ -196,12 +211,11 @@ def anneal_batch_sim(kernel: Kernel, machine: MachineConfig, cfg: AnnealConfig, 
         t0 = float(summ["t0"][c])
         if t0 <= 0:
             raise InvalidBaseline(f"baseline measurement {t0} is not positive")
-        bk = _permuted(kernel, best[c]) if want_schedules else None
-        ck = _permuted(kernel, cur[c]) if want_schedules else None
-        out.append(AnnealState(bk, float(summ["best_energy"][c]), ck,
+        out.append(AnnealState(None, float(summ["best_energy"][c]), None,
                                float(summ["current_energy"][c]), t0, "cycles", len(temps),
-                               records=hist[c], temps=temps,
+                               records=hist[c], temps=temps, base=kernel,
                                best_perm=None if best is None else best[c],
+                               current_perm=None if cur is None else cur[c],
                                ambiguous=int(summ["ambiguous"][c])))
     return out
 
@@ -251,10 +265,9 @@ def anneal_steps(kernel: Kernel, backend, cfg: AnnealConfig, seeds, *,
             on_epoch(chains, rnd)
     hist, best, cur, summ = chains.result()
     unit = getattr(backend, "unit", "")
-    return [AnnealState(_permuted(kernel, best[c]), float(summ["best_energy"][c]),
-                        _permuted(kernel, cur[c]), float(summ["current_energy"][c]), t0[c], unit,
-                        len(temps), records=hist[c], temps=temps, best_perm=best[c],
-                        ambiguous=int(summ["ambiguous"][c]))
+    return [AnnealState(None, float(summ["best_energy"][c]), None, float(summ["current_energy"][c]),
+                        t0[c], unit, len(temps), records=hist[c], temps=temps, base=kernel,
+                        best_perm=best[c], current_perm=cur[c], ambiguous=int(summ["ambiguous"][c]))
             for c in range(C)]
 
 

@@ -68,5 +68,7 @@ struct KernelDev {
 struct sip_kernel {
   sip_ctx* ctx = nullptr;
   sip::KernelDev d;
-  int64_t baseline = 0;  // identity-schedule scoreboard total
+  int64_t baseline = 0;         // identity-schedule scoreboard total
+  struct sip_chains* ws = nullptr;  // reusable chain workspace of sip_anneal_ex
+  uint32_t* d_base = nullptr;   // MT19937 init_genrand(19650218) state
 };

@@ -214,6 +214,12 @@ struct Chains {
   const double* temps = nullptr;
   const int64_t* seeds = nullptr;
   uint16_t* cand_out = nullptr;  // [C][n] chain-major candidate schedules (step mode)
+  const uint16_t* start = nullptr;  // optional start schedule (identity when null)
+  int nck = 0;                      // scoreboard checkpoints per chain (every CK positions)
+  int32_t* ckpt = nullptr;          // [nck][8][C] state of the current schedule
+  int32_t* ckpt2 = nullptr;         // [nck][8][C] state of the candidate being priced
+  int64_t* replayed = nullptr;      // [C] scoreboard steps executed (instrumentation)
+  int32_t* priced = nullptr;        // [C] priced iterations
 };
 
 __device__ __forceinline__ void record(const Chains& s, int c, int it, int status, double t, int lo,
@@ -291,14 +297,105 @@ __device__ Staged stage_tables(const KernelDev& d, bool use_smem) {
 
 __device__ void chain_init(const KernelDev& d, const Chains& s, int c, const uint32_t* base,
                            MtRef& mt) {
+  int j = 0;
   for (int p = 0; p < s.n; ++p) {
-    s.sched[(size_t)p * s.C + c] = (uint16_t)p;
-    s.best[(size_t)p * s.C + c] = (uint16_t)p;
+    uint16_t x = s.start ? s.start[p] : (uint16_t)p;
+    s.sched[(size_t)p * s.C + c] = x;
+    s.best[(size_t)p * s.C + c] = x;
+    if (d.gid[x] >= 0) s.cpos[(size_t)(j++) * s.C + c] = (uint16_t)p;
   }
-  for (int j = 0; j < s.k; ++j) s.cpos[(size_t)j * s.C + c] = (uint16_t)d.gids[j];
   uint32_t key[2];
   int klen = mt_key_from_int(s.seeds[c], key);
   mt_init_by_array(mt, base, key, klen);
+}
+
+// ---- checkpointed scoreboard replay -----------------------------------------
+// The state before every CK-th position of the chain's current schedule is
+// kept (ptr, fin, 6 barrier clocks).  A candidate that swaps (lo, lo+1)
+// replays from the checkpoint below lo only, and stops as soon as its state
+// equals the current schedule's checkpoint further down: barrier clocks are
+// compared as max(clock, ptr), since a clock at or below the issue pointer
+// can never delay an issue again.  From that point both schedules issue
+// identically, so the candidate's total is the current total -- the replay
+// is exact, not an estimate (checked bit for bit against the oracle).
+constexpr int CK = 32;
+
+__device__ __forceinline__ void ck_put(int32_t* base, int C, int c, int j, const Sb& st) {
+  size_t i = (size_t)j * 8 * C + c;
+  base[i] = st.ptr;
+  base[i + C] = st.fin;
+#pragma unroll
+  for (int b = 0; b < 6; ++b) base[i + (size_t)(2 + b) * C] = st.clr[b];
+}
+
+__device__ __forceinline__ void ck_get(const int32_t* base, int C, int c, int j, Sb& st) {
+  size_t i = (size_t)j * 8 * C + c;
+  st.ptr = base[i];
+  st.fin = base[i + C];
+#pragma unroll
+  for (int b = 0; b < 6; ++b) st.clr[b] = base[i + (size_t)(2 + b) * C];
+}
+
+__device__ __forceinline__ bool ck_same(const int32_t* base, int C, int c, int j, const Sb& st) {
+  size_t i = (size_t)j * 8 * C + c;
+  int ptr = base[i];
+  if (ptr != st.ptr || base[i + C] != st.fin) return false;
+#pragma unroll
+  for (int b = 0; b < 6; ++b)
+    if (max(base[i + (size_t)(2 + b) * C], ptr) != max(st.clr[b], ptr)) return false;
+  return true;
+}
+
+// full replay of the chain's current schedule, writing every checkpoint
+__device__ int ck_rebuild(const uint2* meta, const Chains& s, int c) {
+  Sb st;
+  st.reset();
+  const uint16_t* col = s.sched + c;
+  for (int p = 0; p < s.n; ++p) {
+    if (p % CK == 0) ck_put(s.ckpt, s.C, c, p / CK, st);
+    st.step(meta[col[(size_t)p * s.C]]);
+  }
+  return st.total();
+}
+
+// total of the current schedule with (lo, lo+1) exchanged; jconv = first
+// checkpoint where the candidate rejoined the current trajectory (nck if never)
+__device__ int ck_price(const uint2* meta, const Chains& s, int c, int lo, int total_x, int& jconv,
+                        int64_t& steps) {
+  const uint16_t* col = s.sched + c;
+  const int C = s.C, n = s.n;
+  int j0 = lo / CK;
+  Sb st;
+  ck_get(s.ckpt, C, c, j0, st);
+  int p = j0 * CK;
+  for (; p < lo; ++p) st.step(meta[col[(size_t)p * C]]);
+  st.step(meta[col[(size_t)(lo + 1) * C]]);
+  if ((lo + 1) % CK == 0) ck_put(s.ckpt2, C, c, (lo + 1) / CK, st);
+  st.step(meta[col[(size_t)lo * C]]);
+  steps += (lo - j0 * CK) + 2;
+  for (p = lo + 2; p < n; ++p) {
+    if (p % CK == 0) {
+      int j = p / CK;
+      if (ck_same(s.ckpt, C, c, j, st)) {
+        jconv = j;
+        return total_x;
+      }
+      ck_put(s.ckpt2, C, c, j, st);
+    }
+    st.step(meta[col[(size_t)p * C]]);
+    ++steps;
+  }
+  jconv = s.nck;
+  return st.total();
+}
+
+// adopt the priced candidate's checkpoints (those past lo, before jconv)
+__device__ void ck_commit(const Chains& s, int c, int lo, int jconv) {
+  for (int j = (lo + CK) / CK; j < jconv; ++j) {
+    size_t i = (size_t)j * 8 * s.C + c;
+#pragma unroll
+    for (int f = 0; f < 8; ++f) s.ckpt[i + (size_t)f * s.C] = s.ckpt2[i + (size_t)f * s.C];
+  }
 }
 
 // ---- fused simulator-energy annealing: whole chain in one launch ----------
@@ -311,8 +408,10 @@ __global__ void __launch_bounds__(128) anneal_fused_kernel(KernelDev d, Chains s
   MtRef mt{s.mt + c, s.C, MT_N};
   chain_init(d, s, c, mt_base, mt);
   const double t0 = t0_cycles;
-  double e_x = 1.0, e_best = 1.0;
-  int best_iter = -1, amb = 0;
+  int total_x = ck_rebuild(tb.meta, s, c);
+  int64_t steps = s.n;
+  double e_x = (double)total_x / t0, e_best = e_x;
+  int best_iter = -1, amb = 0, priced = 0;
   for (int it = 0; it < s.budget; ++it) {
     int cand, dir, lo;
     int st = propose(d, tb.meta, tb.gid, s, c, mt, cand, dir, lo);
@@ -320,12 +419,17 @@ __global__ void __launch_bounds__(128) anneal_fused_kernel(KernelDev d, Chains s
       record(s, c, it, st, 0.0, lo, cand, dir);
       continue;
     }
-    double t = (double)sim_swapped(tb.meta, s.sched, s.C, c, s.n, lo);
+    ++priced;
+    int jconv;
+    int tc = ck_price(tb.meta, s, c, lo, total_x, jconv, steps);
+    double t = (double)tc;
     double e_c = t / t0;
     double de = e_c - e_x;
     bool acc = metropolis(de, s.temps[it], mt, amb);
     if (acc) {
       apply_swap(tb.gid, s, c, lo, cand, dir);
+      ck_commit(s, c, lo, jconv);
+      total_x = tc;
       e_x = e_c;
       if (de < 0 && e_c < e_best) {
         e_best = e_c;
@@ -341,6 +445,8 @@ __global__ void __launch_bounds__(128) anneal_fused_kernel(KernelDev d, Chains s
   s.best_iter[c] = best_iter;
   s.ambiguous[c] = amb;
   s.mti[c] = mt.mti;
+  s.replayed[c] = steps;
+  s.priced[c] = priced;
 }
 
 // ---- step mode: externally priced candidates -------------------------------
@@ -435,6 +541,21 @@ __global__ void chains_adopt_kernel(KernelDev d, Chains s, const uint16_t* sched
     if (d.gid[x] >= 0) s.cpos[(size_t)(j++) * s.C + c] = (uint16_t)p;
   }
   s.e_x[c] = energy;
+}
+
+// [n][C] -> [C][n] through a 32x32 shared-memory tile (coalesced on both sides)
+__global__ void transpose_u16_kernel(const uint16_t* in, int n, int C, uint16_t* out) {
+  __shared__ uint16_t tile[32][33];
+  int c0 = blockIdx.x * 32, p0 = blockIdx.y * 32;
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    int p = p0 + dy, c = c0 + threadIdx.x;
+    if (p < n && c < C) tile[dy][threadIdx.x] = in[(size_t)p * C + c];
+  }
+  __syncthreads();
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    int c = c0 + dy, p = p0 + threadIdx.x;
+    if (p < n && c < C) out[(size_t)c * n + p] = tile[threadIdx.x][dy];
+  }
 }
 
 // ---- API helpers: batch simulate + legality queries ------------------------
@@ -547,6 +668,7 @@ struct sip_chains {
   uint8_t* d_status = nullptr;
   int32_t* d_lo = nullptr;
   uint16_t* d_adopt = nullptr;
+  uint16_t* d_start = nullptr;
 };
 
 static int chains_alloc(sip_ctx* ctx, sip_kernel* k, const sip_anneal_cfg* cfg, int chains,
@@ -575,8 +697,17 @@ static int chains_alloc(sip_ctx* ctx, sip_kernel* k, const sip_anneal_cfg* cfg, 
   TRY(dalloc(ctx, &s.p_cand, C));
   TRY(dalloc(ctx, &s.p_dir, C));
   TRY(dalloc(ctx, &s.hist, (size_t)std::max(s.budget, 1) * C));
+  s.nck = (s.n + CK - 1) / CK;
+  TRY(dalloc(ctx, &s.ckpt, (size_t)s.nck * 8 * C));
+  TRY(dalloc(ctx, &s.ckpt2, (size_t)s.nck * 8 * C));
+  TRY(dalloc(ctx, &s.replayed, C));
+  TRY(dalloc(ctx, &s.priced, C));
+  SIP_CUDA(ctx, cudaMemsetAsync(s.replayed, 0, sizeof(int64_t) * C, ctx->stream));
+  SIP_CUDA(ctx, cudaMemsetAsync(s.priced, 0, sizeof(int32_t) * C, ctx->stream));
   TRY(dalloc(ctx, &o->d_temps, (size_t)std::max(s.budget, 1)));
   TRY(dalloc(ctx, &o->d_seeds, C));
+  SIP_CUDA(ctx, cudaMemsetAsync(s.hist, 0xFF, sizeof(sip_record) * (size_t)std::max(s.budget, 1) * C,
+                                ctx->stream));  // status 255 = iteration not run yet
   TRY(h2d(ctx, o->d_temps, cfg->temperature, (size_t)s.budget));
   TRY(h2d(ctx, o->d_seeds, seeds, C));
   s.temps = o->d_temps;
@@ -588,19 +719,25 @@ static void chains_free(sip_chains* o) {
   Chains& s = o->s;
   void* ptrs[] = {s.sched, s.best, s.cpos, s.mt, s.mti, s.t0, s.e_x, s.e_best, s.it,
                   s.best_iter, s.ambiguous, s.p_lo, s.p_cand, s.p_dir, s.hist, o->d_temps,
-                  o->d_seeds, o->d_tcurr, o->d_status, o->d_lo, s.cand_out, o->d_adopt};
+                  o->d_seeds, o->d_tcurr, o->d_status, o->d_lo, s.cand_out, o->d_adopt,
+                  s.ckpt, s.ckpt2, s.replayed, s.priced, o->d_start};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
 
 // transpose position-major [n][C] device array into chain-major host [C][n]
 static int fetch_sched(sip_ctx* ctx, const uint16_t* dsrc, int n, int C, uint16_t* host) {
-  std::vector<uint16_t> tmp((size_t)n * C);
-  TRY(d2h(ctx, tmp.data(), dsrc, tmp.size()));
-  SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  for (int p = 0; p < n; ++p)
-    for (int c = 0; c < C; ++c) host[(size_t)c * n + p] = tmp[(size_t)p * C + c];
-  return SIP_OK;
+  uint16_t* tmp = nullptr;
+  TRY(dalloc(ctx, &tmp, (size_t)n * C));
+  dim3 grid((C + 31) / 32, (n + 31) / 32);
+  transpose_u16_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(dsrc, n, C, tmp);
+  int rc = SIP_OK;
+  if (cudaGetLastError() != cudaSuccess) rc = fail(ctx, SIP_E_CUDA, "transpose launch failed");
+  if (rc == SIP_OK) rc = d2h(ctx, host, tmp, (size_t)n * C);
+  if (rc == SIP_OK && cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+    rc = fail(ctx, SIP_E_CUDA, "schedule fetch failed");
+  cudaFree(tmp);
+  return rc;
 }
 
 static int chains_fetch(sip_chains* o, sip_record* history, uint16_t* best, uint16_t* current,
@@ -614,6 +751,10 @@ static int chains_fetch(sip_chains* o, sip_record* history, uint16_t* best, uint
   if (summary) {
     std::vector<double> t0(C), ex(C), eb(C);
     std::vector<int32_t> bi(C), am(C);
+    std::vector<int64_t> rp(C, 0);
+    std::vector<int32_t> pr(C, 0);
+    if (s.replayed) TRY(d2h(ctx, rp.data(), s.replayed, C));
+    if (s.priced) TRY(d2h(ctx, pr.data(), s.priced, C));
     TRY(d2h(ctx, t0.data(), s.t0, C));
     TRY(d2h(ctx, ex.data(), s.e_x, C));
     TRY(d2h(ctx, eb.data(), s.e_best, C));
@@ -621,7 +762,7 @@ static int chains_fetch(sip_chains* o, sip_record* history, uint16_t* best, uint
     TRY(d2h(ctx, am.data(), s.ambiguous, C));
     SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     for (size_t c = 0; c < C; ++c)
-      summary[c] = sip_chain_summary{t0[c], eb[c], ex[c], bi[c], am[c]};
+      summary[c] = sip_chain_summary{t0[c], eb[c], ex[c], bi[c], am[c], rp[c], pr[c], 0};
   }
   SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return SIP_OK;
@@ -713,6 +854,11 @@ int sip_kernel_create(sip_ctx* ctx, const sip_tables* t, sip_kernel** out) {
 
 int sip_kernel_destroy(sip_kernel* k) {
   if (!k) return SIP_OK;
+  if (k->ws) {
+    chains_free(k->ws);
+    delete k->ws;
+  }
+  if (k->d_base) cudaFree(k->d_base);
   KernelDev& d = k->d;
   void* ptrs[] = {d.meta, d.klass, d.reads, d.writes, d.refs, d.nrefs, d.cut,
                   d.pin,  d.gid,   d.gids,  d.e_after, d.e_before};
@@ -800,32 +946,80 @@ done:
   return rc;
 }
 
-int sip_anneal(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds, int32_t chains,
-               sip_record* history, uint16_t* best, uint16_t* current, sip_chain_summary* summary) {
+int sip_anneal_ex(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds, int32_t chains,
+                  const uint16_t* start, sip_record* history, uint16_t* best, uint16_t* current,
+                  sip_chain_summary* summary, uint16_t* champion, int32_t* champion_chain) {
   if (!k || !cfg || !seeds || chains < 1 || cfg->budget < 0) return SIP_E_ARG;
   sip_ctx* ctx = k->ctx;
   if (k->d.k == 0) return fail(ctx, SIP_E_NOCAND, "no global-memory instructions to move");
-  sip_chains o;
-  o.k = k;
-  int rc = chains_alloc(ctx, k, cfg, chains, seeds, &o);
-  uint32_t* d_base = nullptr;
-  if (rc == SIP_OK) rc = dalloc(ctx, &d_base, MT_N);
-  if (rc == SIP_OK) rc = h2d(ctx, d_base, mt_base_host().data(), MT_N);
-  if (rc == SIP_OK) {
-    size_t sm = smem_need(k->d);
-    int use_smem = sm <= kSmemCap;
-    if (use_smem) rc = configure_smem(ctx, (const void*)anneal_fused_kernel, sm);
-    if (rc == SIP_OK) {
-      anneal_fused_kernel<<<(chains + 127) / 128, 128, use_smem ? sm : 0, ctx->stream>>>(
-          k->d, o.s, d_base, use_smem, (double)k->baseline);
-      cudaError_t e = cudaGetLastError();
-      if (e != cudaSuccess) rc = fail(ctx, SIP_E_CUDA, std::string("anneal: ") + cudaGetErrorString(e));
-    }
+  // chain state lives in a per-listing workspace reused across calls of the same shape
+  if (k->ws && (k->ws->s.C != chains || k->ws->s.budget != cfg->budget)) {
+    chains_free(k->ws);
+    delete k->ws;
+    k->ws = nullptr;
   }
-  if (rc == SIP_OK) rc = chains_fetch(&o, history, best, current, summary);
-  if (d_base) cudaFree(d_base);
-  chains_free(&o);
-  return rc;
+  int rc = SIP_OK;
+  if (!k->ws) {
+    k->ws = new sip_chains();
+    k->ws->k = k;
+    rc = chains_alloc(ctx, k, cfg, chains, seeds, k->ws);
+    if (rc != SIP_OK) {
+      chains_free(k->ws);
+      delete k->ws;
+      k->ws = nullptr;
+      return rc;
+    }
+  } else {
+    Chains& s = k->ws->s;
+    s.unsafe = cfg->unsafe_moves;
+    s.hw_safe = cfg->hw_safe;
+    s.minfix = cfg->min_fixed_distance;
+    TRY(h2d(ctx, k->ws->d_temps, cfg->temperature, (size_t)s.budget));
+    TRY(h2d(ctx, k->ws->d_seeds, seeds, (size_t)chains));
+  }
+  sip_chains& o = *k->ws;
+  if (!k->d_base) {
+    TRY(dalloc(ctx, &k->d_base, MT_N));
+    TRY(h2d(ctx, k->d_base, mt_base_host().data(), MT_N));
+  }
+  o.s.start = nullptr;
+  if (start) {
+    if (!o.d_start) TRY(dalloc(ctx, &o.d_start, (size_t)o.s.n));
+    TRY(h2d(ctx, o.d_start, start, (size_t)o.s.n));
+    o.s.start = o.d_start;
+  }
+  size_t sm = smem_need(k->d);
+  int use_smem = sm <= kSmemCap;
+  if (use_smem) TRY(configure_smem(ctx, (const void*)anneal_fused_kernel, sm));
+  anneal_fused_kernel<<<(chains + 127) / 128, 128, use_smem ? sm : 0, ctx->stream>>>(
+      k->d, o.s, k->d_base, use_smem, (double)k->baseline);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ctx, SIP_E_CUDA, std::string("anneal: ") + cudaGetErrorString(e));
+  std::vector<sip_chain_summary> tmp;
+  sip_chain_summary* sum = summary;
+  if (!sum && champion) {
+    tmp.resize(chains);
+    sum = tmp.data();
+  }
+  TRY(chains_fetch(&o, history, best, current, sum));
+  if (champion) {  // ranked like driver.py:81-85: (best energy, seed)
+    int w = 0;
+    for (int c = 1; c < chains; ++c)
+      if (sum[c].best_energy < sum[w].best_energy ||
+          (sum[c].best_energy == sum[w].best_energy && seeds[c] < seeds[w]))
+        w = c;
+    SIP_CUDA(ctx, cudaMemcpy2DAsync(champion, sizeof(uint16_t), o.s.best + w, sizeof(uint16_t) * chains,
+                                    sizeof(uint16_t), (size_t)o.s.n, cudaMemcpyDeviceToHost, ctx->stream));
+    SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (champion_chain) *champion_chain = w;
+  }
+  return SIP_OK;
+}
+
+int sip_anneal(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds, int32_t chains,
+               sip_record* history, uint16_t* best, uint16_t* current, sip_chain_summary* summary) {
+  return sip_anneal_ex(k, cfg, seeds, chains, nullptr, history, best, current, summary, nullptr,
+                       nullptr);
 }
 
 int sip_chains_create(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds,

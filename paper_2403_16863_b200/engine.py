@@ -58,7 +58,8 @@ class AnnealCfg(ctypes.Structure):
 RECORD_DTYPE = np.dtype([("time", "<f8"), ("lo", "<i4"), ("candidate", "<u2"),
                          ("direction", "u1"), ("status", "u1")])
 SUMMARY_DTYPE = np.dtype([("t0", "<f8"), ("best_energy", "<f8"), ("current_energy", "<f8"),
-                          ("best_iter", "<i4"), ("ambiguous", "<i4")])
+                          ("best_iter", "<i4"), ("ambiguous", "<i4"), ("replayed", "<i8"),
+                          ("priced", "<i4"), ("pad", "<i4")])
 
 
 class Launch(ctypes.Structure):
@@ -95,6 +96,8 @@ _SIGS = {
                       ctypes.POINTER(ctypes.c_int8)], ctypes.c_int),
     "sip_anneal": ([ctypes.c_void_p, ctypes.POINTER(AnnealCfg), c_i64p, ctypes.c_int32,
                     ctypes.c_void_p, c_u16p, c_u16p, ctypes.c_void_p], ctypes.c_int),
+    "sip_anneal_ex": ([ctypes.c_void_p, ctypes.POINTER(AnnealCfg), c_i64p, ctypes.c_int32, c_u16p,
+                       ctypes.c_void_p, c_u16p, c_u16p, ctypes.c_void_p, c_u16p, c_i32p], ctypes.c_int),
     "sip_chains_create": ([ctypes.c_void_p, ctypes.POINTER(AnnealCfg), c_i64p, c_dblp,
                            ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
     "sip_chains_propose": ([ctypes.c_void_p, c_i32p, c_u16p], ctypes.c_int),
@@ -300,6 +303,26 @@ class DeviceKernel:
                                                hist.ctypes.data_as(ctypes.c_void_p), bp, cp,
                                                summ.ctypes.data_as(ctypes.c_void_p)))
         return hist, best, cur, summ
+
+    def anneal_epoch(self, seeds, temps: np.ndarray, start=None, unsafe: bool = False,
+                     with_history: bool = True):
+        """Fused chains from `start` (identity if None); returns (history|None, summary,
+        champion schedule, champion chain).  Schedules of other chains stay on the device."""
+        seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.int64))
+        temps = np.ascontiguousarray(temps, dtype=np.float64)
+        C, B = len(seeds), len(temps)
+        hist = np.zeros((C, B), dtype=RECORD_DTYPE) if with_history else None
+        summ = np.zeros(C, dtype=SUMMARY_DTYPE)
+        champ = np.zeros(self.n, dtype=np.uint16)
+        wch = ctypes.c_int32(-1)
+        st = None if start is None else np.ascontiguousarray(start, dtype=np.uint16)
+        cfg = self._cfg(temps, unsafe, False, 0)
+        self.ctx.check(self.ctx.lib.sip_anneal_ex(
+            self.handle, ctypes.byref(cfg), _ptr(seeds, c_i64p), C,
+            None if st is None else _ptr(st, c_u16p),
+            None if hist is None else hist.ctypes.data_as(ctypes.c_void_p), None, None,
+            summ.ctypes.data_as(ctypes.c_void_p), _ptr(champ, c_u16p), ctypes.byref(wch)))
+        return hist, summ, champ, wch.value
 
     def chains(self, seeds, t0, temps: np.ndarray, unsafe: bool = False, hw_safe: bool = False,
                min_fixed: int = 0) -> "StepChains":

@@ -1,0 +1,108 @@
+"""Hardware-energy search: many annealing chains per GPU, priced on the B200.
+
+One process per GPU.  Each rank owns ``chains`` step-mode chains on its
+device (``sip_chains_*``): every round the device proposes one legal move per
+live chain (hw_safe legality), the evaluator times each candidate
+(``sip_measure``), and the device applies the Metropolis rule.  Every
+``epoch`` rounds the ranks all-gather their best (energy, seed) records over
+NCCL and every chain adopts the global best schedule (the owner broadcasts
+it) -- the north star's "allgather of (cost, schedule-id) each epoch".  With
+one rank and exchange disabled this is exactly ``driver.run_search`` with a
+``B200Backend``, chain for chain.
+
+Reference anchors: chains with consecutive seeds (driver.py:73-79); ranking by
+(best_time, seed) (driver.py:81-85); Metropolis/feedback (anneal.py:28-44).
+"""
+from __future__ import annotations
+
+from dataclasses import replace
+
+import numpy as np
+
+from .anneal import AnnealConfig
+from .driver import hardware_config
+from .engine import ST_ACCEPTED, ST_MEASURE, ST_PRICED
+from .backends import MeasurementFailed
+
+
+class HardwareSearch:
+    def __init__(self, backend, cfg: AnnealConfig, chains: int, *, seed0: int | None = None,
+                 epoch: int = 0, dist=None):
+        self.be = backend
+        self.cfg = hardware_config(backend, cfg)
+        self.kernel = backend.kernel
+        self.tables = backend.tables_for(self.kernel)
+        self.dk = backend.ctx.kernel(self.tables)
+        self.dist = dist  # torch.distributed module when world_size > 1
+        self.rank = dist.get_rank() if dist else 0
+        self.world = dist.get_world_size() if dist else 1
+        base = cfg.seed if seed0 is None else seed0
+        self.seeds = [base + self.rank * chains + c for c in range(chains)]
+        self.C = chains
+        self.epoch = epoch
+        self.rounds = 0
+        self.evaluated = 0
+        self.proposals_seen = 0
+        ident = np.arange(self.dk.n, dtype=np.uint16)
+        t0 = backend.measure_perm(ident, self.cfg.measure_reps).value
+        self.t0 = t0
+        self.temps = self.cfg.temperatures()
+        self.chains = self.dk.chains(self.seeds, [t0] * chains, self.temps, self.cfg.unsafe_moves,
+                                     self.cfg.hw_safe, self.cfg.min_fixed_distance)
+        self.times = np.zeros(chains, dtype=np.float64)
+        self.status = np.zeros(chains, dtype=np.uint8)
+        self.launches = 0  # device kernels launched by this search (propose/resolve/evaluated runs)
+
+    def step(self) -> int:
+        """One round: propose, price every legal candidate, resolve.  Returns #priced."""
+        lo, cand = self.chains.propose(with_schedules=True)
+        self.launches += 1
+        live = np.nonzero(lo >= 0)[0]
+        n = 0
+        for c in live:
+            try:
+                self.times[c] = self.be.measure_perm(cand[c], self.cfg.measure_reps).value
+                self.status[c] = ST_PRICED
+                n += 1
+                self.launches += self.be.warmup + self.cfg.measure_reps
+            except MeasurementFailed:
+                self.times[c], self.status[c] = 0.0, ST_MEASURE
+        if len(live):
+            self.chains.resolve(self.times, self.status)
+            self.launches += 1
+        self.rounds += 1
+        self.evaluated += n
+        if self.epoch and self.rounds % self.epoch == 0:
+            self.exchange()
+        return n
+
+    def local_best(self):
+        hist, best, cur, summ = self.chains.result()
+        key = [(float(summ["best_energy"][c]), self.seeds[c]) for c in range(self.C)]
+        c = min(range(self.C), key=lambda i: key[i])
+        return key[c][0], key[c][1], best[c], hist, summ
+
+    def exchange(self) -> None:
+        """All-gather (energy, seed) per rank; every chain adopts the global best."""
+        e, seed, sched, _, _ = self.local_best()
+        if self.dist is None:
+            self.chains.adopt(sched, e, e * self.t0)
+            return
+        import torch
+
+        dev = torch.device("cuda", self.be.device)
+        mine = torch.tensor([e, float(seed), float(self.rank)], dtype=torch.float64, device=dev)
+        allv = [torch.zeros_like(mine) for _ in range(self.world)]
+        self.dist.all_gather(allv, mine)
+        rows = sorted((float(v[0]), float(v[1]), int(v[2])) for v in allv)
+        be, bs, owner = rows[0]
+        buf = torch.as_tensor(sched.astype(np.int32), device=dev)
+        self.dist.broadcast(buf, src=owner)
+        self.chains.adopt(buf.cpu().numpy().astype(np.uint16), be, be * self.t0)
+
+    def result(self):
+        e, seed, sched, hist, summ = self.local_best()
+        priced = int(np.count_nonzero(hist["status"] <= ST_PRICED))
+        accepted = int(np.count_nonzero(hist["status"] == ST_ACCEPTED))
+        return {"best_energy": e, "best_seed": seed, "best_perm": sched, "priced": priced,
+                "accepted": accepted, "t0_ms": self.t0, "summary": summ}

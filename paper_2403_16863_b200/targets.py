@@ -88,14 +88,16 @@ class GemmTarget:
     def output(self):
         return self._bufs["C"]
 
-    def launch(self) -> tuple:
-        """(Launch struct, params buffer) for the current buffers."""
+    def launch(self, out=None) -> tuple:
+        """(Launch struct, params buffer) for the current buffers (output `out` or C)."""
         if not self._bufs:
             self.allocate()
         ctx = get_context(self.device)
         lp = Launch()
         params = ctypes.create_string_buffer(512)
         A, B, C = (self._bufs[k] for k in "ABC")
+        if out is not None:
+            C = out
         ctx.check(ctx.lib.sip_target_gemm_launch(
             ctx.handle, ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(B.data_ptr()),
             ctypes.c_void_p(C.data_ptr()), self.M, self.N, self.K, self.L, ctypes.c_float(self.slope),

@@ -1,0 +1,123 @@
+"""Probabilistic verification of a candidate schedule on real hardware (G5/G6).
+
+Semantics follow the reference's differential testing (difftest.py:158-204)
+and the paper's 10M-sample check: a *sample* is one
+independent random input; the baseline (nvcc) schedule and the candidate run
+on it and their outputs are compared.  Here one launch of the target covers
+``batch`` samples at once (the targets take a batch dimension), inputs come
+from libsip's Philox generator (stream = batch index), and the comparison is
+the HBM-bound ``sip_compare`` kernel.  The verdict fails on any element with
+|cand - ref| > atol + rtol * |ref|; bit-level differences are counted too
+(a pure reordering is expected to be bit-identical).
+"""
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from .backends import MeasurementFailed
+from .cubin import Module
+from .engine import SIP_E_MEASURE, CmpResult, c_u16p, get_context
+
+# verification shape per target: one sample = one independent problem of this size
+VERIFY_SHAPES = {
+    "gemm": dict(M=256, N=256, K=1024),
+    "attn": dict(B=1, H=1, S=256, D=128),
+}
+DEFAULT_BATCH = {"gemm": 1024, "attn": 512}
+TOLERANCE = {"fp16": (1e-2, 1e-2)}
+
+
+@dataclass
+class VerifyResult:
+    samples: int
+    passed: int
+    failed: int
+    first_fail_sample: int
+    first_fail_elem: int
+    bitdiff_elems: int
+    mismatched_elems: int
+    max_abs_err: float
+    seconds: float
+    compared_bytes: int
+
+    @property
+    def ok(self) -> bool:
+        return self.failed == 0
+
+    def to_dict(self) -> dict:
+        return {k: getattr(self, k) for k in self.__dataclass_fields__} | {"ok": self.ok}
+
+
+class Verifier:
+    """Baseline vs candidate over many samples for one target kind."""
+
+    def __init__(self, kind: str, *, device: int = 0, batch: int | None = None, seed: int = 0,
+                 shape: dict | None = None):
+        from .targets import make_target
+
+        self.kind = kind
+        self.ctx = get_context(device)
+        self.batch = batch or DEFAULT_BATCH[kind]
+        sh = dict(VERIFY_SHAPES[kind], **(shape or {}))
+        if kind == "gemm":
+            self.target = make_target("gemm", L=self.batch, seed=seed, device=device, **sh).allocate()
+        else:
+            self.target = make_target("attn", seed=seed, device=device, **sh)
+            self.target.B *= self.batch
+            self.target.allocate()
+        cubin, func = self.target.cubin()
+        self.module = Module(cubin, func, ctx=self.ctx)
+        self.out_ref = self.target.output
+        self.out_cand = self.out_ref.clone()
+        self.launch_ref, self._p1 = self.target.launch(out=self.out_ref)
+        self.launch_cand, self._p2 = self.target.launch(out=self.out_cand)
+        self.elems_per_sample = self.out_ref.numel() // self.batch
+        self.atol, self.rtol = TOLERANCE["fp16"]
+
+    def _run(self, perm, launch) -> None:
+        lib = self.ctx.lib
+        p = None if perm is None else np.ascontiguousarray(perm, dtype=np.uint16)
+        rc = lib.sip_run(self.module.handle, None if p is None else p.ctypes.data_as(c_u16p),
+                         ctypes.byref(launch))
+        if rc == SIP_E_MEASURE:
+            raise MeasurementFailed(lib.sip_last_error(self.ctx.handle).decode(errors="replace"))
+        self.ctx.check(rc)
+
+    def run(self, perm, samples: int, *, first_batch: int = 0, batch_stride: int = 1,
+            fail_fast: bool = False) -> VerifyResult:
+        """Verify `perm` on batches first_batch, first_batch+stride, ... covering `samples`."""
+        t0 = time.perf_counter()
+        nb = (samples + self.batch - 1) // self.batch
+        passed = failed = bitdiff = mism = 0
+        first_s, first_e, maxerr = -1, -1, 0.0
+        done = 0
+        lib = self.ctx.lib
+        res = CmpResult()
+        for i in range(nb):
+            j = first_batch + i * batch_stride
+            self.target.fill(stream=j)
+            self._run(None, self.launch_ref)
+            self._run(perm, self.launch_cand)
+            rc = lib.sip_compare(self.ctx.handle, ctypes.c_void_p(self.out_ref.data_ptr()),
+                                 ctypes.c_void_p(self.out_cand.data_ptr()), self.out_ref.numel(), 0,
+                                 self.atol, self.rtol, self.elems_per_sample, j * self.batch,
+                                 ctypes.byref(res))
+            self.ctx.check(rc)
+            n_here = min(self.batch, samples - done)
+            done += n_here
+            failed += min(res.failed_samples, n_here)
+            passed += n_here - min(res.failed_samples, n_here)
+            bitdiff += res.bitdiff_elems
+            mism += res.mismatched_elems
+            maxerr = max(maxerr, res.max_abs_err)
+            if res.first_fail_sample >= 0 and (first_s < 0 or res.first_fail_sample < first_s):
+                first_s, first_e = res.first_fail_sample, res.first_fail_elem
+            if fail_fast and failed:
+                break
+        dt = time.perf_counter() - t0
+        nbytes = 2 * 2 * self.out_ref.numel() * (i + 1)
+        return VerifyResult(done, passed, failed, first_s, first_e, bitdiff, mism, maxerr, dt, nbytes)
