@@ -261,6 +261,7 @@ def main() -> None:
     from paper_2403_16863_b200.evaluator import B200Backend
     from paper_2403_16863_b200.hwsearch import HardwareSearch
     from paper_2403_16863_b200.machine import MachineConfig
+    from paper_2403_16863_b200.parallel import exchange_best
     from paper_2403_16863_b200.tables import KernelTables
     from paper_2403_16863_b200.targets import GemmTarget
     from paper_2403_16863_b200.verify import Verifier
@@ -283,13 +284,7 @@ def main() -> None:
         i = int(np.lexsort((seeds, summ["best_energy"]))[0])
         e_mine = float(summ["best_energy"][i])
         if dist:  # NCCL allgather of (energy, seed, rank); owner broadcasts its champion
-            mine = torch.tensor([e_mine, float(seeds[i]), float(rank)], dtype=torch.float64, device="cuda")
-            allv = [torch.zeros_like(mine) for _ in range(world)]
-            dist.all_gather(allv, mine)
-            e_g, _, owner = sorted(tuple(float(x) for x in v.tolist()) for v in allv)[0]
-            buf = torch.as_tensor(champ.astype(np.int32), device="cuda")
-            dist.broadcast(buf, src=int(owner))
-            champ, e_mine = buf.cpu().numpy().astype(np.uint16), e_g
+            e_mine, _, _, champ = exchange_best(dist, e_mine, int(seeds[i]), champ, torch.device("cuda", local))
         if e_mine < best["e"]:
             best["e"], best["perm"] = e_mine, champ
         return int(summ["priced"].sum()), int(summ["replayed"].sum()), int(summ["ambiguous"].sum())

@@ -176,25 +176,14 @@ struct Sb {
   __device__ __forceinline__ int total() const { return max(fin, ptr); }
 };
 
-// total of the chain's schedule with slots (lo, lo+1) exchanged (lo = -1: as is)
-__device__ int sim_swapped(const uint2* meta, const uint16_t* sched, int C, int c, int n, int lo) {
-  Sb s;
-  s.reset();
-  const uint16_t* col = sched + c;
-  int end0 = lo < 0 ? n : lo;
-  for (int p = 0; p < end0; ++p) s.step(meta[col[(size_t)p * C]]);
-  if (lo >= 0) {
-    s.step(meta[col[(size_t)(lo + 1) * C]]);
-    s.step(meta[col[(size_t)lo * C]]);
-    for (int p = lo + 2; p < n; ++p) s.step(meta[col[(size_t)p * C]]);
-  }
-  return s.total();
-}
-
 // ---------------------------------------------------------------------------
-// chain state (device), position-major [*, C]
+// chain state (device).  Schedules are chain-major rows of `ns` (n rounded up
+// to 8) u16 so a replay streams its own row with 16-byte loads; the MT words,
+// candidate positions and checkpoints are position-major [*, C] (all chains
+// touch the same index in lockstep, so a warp's accesses coalesce).
 struct Chains {
-  int C = 0, n = 0, k = 0, budget = 0;
+  int C = 0, n = 0, ns = 0, k = 0, budget = 0;
+  int record_hist = 1;
   int unsafe = 0, hw_safe = 0, minfix = 0;
   uint16_t* sched = nullptr;
   uint16_t* best = nullptr;
@@ -230,7 +219,7 @@ __device__ __forceinline__ void record(const Chains& s, int c, int it, int statu
   r.candidate = (uint16_t)cand;
   r.direction = (uint8_t)dir;
   r.status = (uint8_t)status;
-  s.hist[(size_t)c * s.budget + it] = r;
+  if (s.record_hist) s.hist[(size_t)c * s.budget + it] = r;
 }
 
 // perturb.sample_action + apply_action checks.  Returns -1 when the move is
@@ -244,18 +233,19 @@ __device__ int propose(const KernelDev& d, const uint2* meta, const int16_t* gid
   lo = dir == 0 ? pos - 1 : pos;
   if (lo < 0 || lo + 1 >= s.n) return SIP_ST_BOUNDARY;
   if (d.cut[lo + 1]) return SIP_ST_BOUNDARY;
-  int a = s.sched[(size_t)lo * s.C + c], b = s.sched[(size_t)(lo + 1) * s.C + c];
+  const uint16_t* row = s.sched + (size_t)c * s.ns;
+  int a = row[lo], b = row[lo + 1];
   if (!s.unsafe && edge_lookup(d, gid, a, b)) return SIP_ST_DEPENDENCY;
   if (s.hw_safe) {
-    auto at = [&](int p) { return (int)s.sched[(size_t)p * s.C + c]; };
+    auto at = [&](int p) { return (int)row[p]; };
     if (!hw_safe_ok(d, meta, at, s.n, lo, a, b, s.minfix)) return SIP_ST_HWSAFE;
   }
   return -1;
 }
 
 __device__ void apply_swap(const int16_t* gid, const Chains& s, int c, int lo, int cand, int dir) {
-  uint16_t* x = s.sched + (size_t)lo * s.C + c;
-  uint16_t* y = s.sched + (size_t)(lo + 1) * s.C + c;
+  uint16_t* x = s.sched + (size_t)c * s.ns + lo;
+  uint16_t* y = x + 1;
   uint16_t a = *x, b = *y;
   *x = b;
   *y = a;
@@ -264,7 +254,9 @@ __device__ void apply_swap(const int16_t* gid, const Chains& s, int c, int lo, i
 }
 
 __device__ void copy_best(const Chains& s, int c) {
-  for (int p = 0; p < s.n; ++p) s.best[(size_t)p * s.C + c] = s.sched[(size_t)p * s.C + c];
+  const uint4* src = reinterpret_cast<const uint4*>(s.sched + (size_t)c * s.ns);
+  uint4* dst = reinterpret_cast<uint4*>(s.best + (size_t)c * s.ns);
+  for (int q = 0; q < s.ns / 8; ++q) dst[q] = src[q];
 }
 
 // Metropolis rule (anneal.py:39-44); counts decisions too close to call.
@@ -300,10 +292,11 @@ __device__ void chain_init(const KernelDev& d, const Chains& s, int c, const uin
   int j = 0;
   for (int p = 0; p < s.n; ++p) {
     uint16_t x = s.start ? s.start[p] : (uint16_t)p;
-    s.sched[(size_t)p * s.C + c] = x;
-    s.best[(size_t)p * s.C + c] = x;
+    s.sched[(size_t)c * s.ns + p] = x;
+    s.best[(size_t)c * s.ns + p] = x;
     if (d.gid[x] >= 0) s.cpos[(size_t)(j++) * s.C + c] = (uint16_t)p;
   }
+  for (int p = s.n; p < s.ns; ++p) s.sched[(size_t)c * s.ns + p] = s.best[(size_t)c * s.ns + p] = 0;
   uint32_t key[2];
   int klen = mt_key_from_int(s.seeds[c], key);
   mt_init_by_array(mt, base, key, klen);
@@ -346,14 +339,34 @@ __device__ __forceinline__ bool ck_same(const int32_t* base, int C, int c, int j
   return true;
 }
 
+// 8 positions per 16-byte load; the 8 table lookups are issued before the
+// serial scoreboard updates so their shared-memory latency overlaps.
+__device__ __forceinline__ void step8(const uint2* meta, uint4 v, Sb& st) {
+  uint2 m[8];
+  m[0] = meta[v.x & 0xffffu]; m[1] = meta[v.x >> 16];
+  m[2] = meta[v.y & 0xffffu]; m[3] = meta[v.y >> 16];
+  m[4] = meta[v.z & 0xffffu]; m[5] = meta[v.z >> 16];
+  m[6] = meta[v.w & 0xffffu]; m[7] = meta[v.w >> 16];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) st.step(m[i]);
+}
+
+// replay positions [p0, p1) of a chain-major row
+__device__ __forceinline__ void replay_span(const uint2* meta, const uint16_t* row, int p0, int p1, Sb& st) {
+  int p = p0;
+  for (; p < p1 && (p & 7); ++p) st.step(meta[row[p]]);
+  for (; p + 8 <= p1; p += 8) step8(meta, *reinterpret_cast<const uint4*>(row + p), st);
+  for (; p < p1; ++p) st.step(meta[row[p]]);
+}
+
 // full replay of the chain's current schedule, writing every checkpoint
 __device__ int ck_rebuild(const uint2* meta, const Chains& s, int c) {
   Sb st;
   st.reset();
-  const uint16_t* col = s.sched + c;
-  for (int p = 0; p < s.n; ++p) {
-    if (p % CK == 0) ck_put(s.ckpt, s.C, c, p / CK, st);
-    st.step(meta[col[(size_t)p * s.C]]);
+  const uint16_t* row = s.sched + (size_t)c * s.ns;
+  for (int j = 0; j < s.nck; ++j) {
+    ck_put(s.ckpt, s.C, c, j, st);
+    replay_span(meta, row, j * CK, min(s.n, (j + 1) * CK), st);
   }
   return st.total();
 }
@@ -362,28 +375,29 @@ __device__ int ck_rebuild(const uint2* meta, const Chains& s, int c) {
 // checkpoint where the candidate rejoined the current trajectory (nck if never)
 __device__ int ck_price(const uint2* meta, const Chains& s, int c, int lo, int total_x, int& jconv,
                         int64_t& steps) {
-  const uint16_t* col = s.sched + c;
+  const uint16_t* row = s.sched + (size_t)c * s.ns;
   const int C = s.C, n = s.n;
   int j0 = lo / CK;
   Sb st;
   ck_get(s.ckpt, C, c, j0, st);
-  int p = j0 * CK;
-  for (; p < lo; ++p) st.step(meta[col[(size_t)p * C]]);
-  st.step(meta[col[(size_t)(lo + 1) * C]]);
+  replay_span(meta, row, j0 * CK, lo, st);
+  st.step(meta[row[lo + 1]]);
   if ((lo + 1) % CK == 0) ck_put(s.ckpt2, C, c, (lo + 1) / CK, st);
-  st.step(meta[col[(size_t)lo * C]]);
-  steps += (lo - j0 * CK) + 2;
-  for (p = lo + 2; p < n; ++p) {
-    if (p % CK == 0) {
-      int j = p / CK;
-      if (ck_same(s.ckpt, C, c, j, st)) {
-        jconv = j;
-        return total_x;
-      }
-      ck_put(s.ckpt2, C, c, j, st);
+  st.step(meta[row[lo]]);
+  int p = lo + 2;
+  int pb = min(n, ((p + CK - 1) / CK) * CK);
+  replay_span(meta, row, p, pb, st);
+  steps += (pb - j0 * CK);
+  for (p = pb; p < n; p += CK) {
+    int j = p / CK;
+    if (ck_same(s.ckpt, C, c, j, st)) {
+      jconv = j;
+      return total_x;
     }
-    st.step(meta[col[(size_t)p * C]]);
-    ++steps;
+    ck_put(s.ckpt2, C, c, j, st);
+    int pe = min(n, p + CK);
+    replay_span(meta, row, p, pe, st);
+    steps += pe - p;
   }
   jconv = s.nck;
   return st.total();
@@ -489,7 +503,8 @@ __global__ void __launch_bounds__(128) chains_propose_kernel(KernelDev d, Chains
   lo_out[c] = lo;
   if (s.cand_out != nullptr && lo >= 0) {
     uint16_t* out = s.cand_out + (size_t)c * s.n;
-    for (int p = 0; p < s.n; ++p) out[p] = s.sched[(size_t)p * s.C + c];
+    const uint16_t* row = s.sched + (size_t)c * s.ns;
+    for (int p = 0; p < s.n; ++p) out[p] = row[p];
     uint16_t t = out[lo];
     out[lo] = out[lo + 1];
     out[lo + 1] = t;
@@ -537,25 +552,10 @@ __global__ void chains_adopt_kernel(KernelDev d, Chains s, const uint16_t* sched
   int j = 0;
   for (int p = 0; p < s.n; ++p) {
     uint16_t x = sched[p];
-    s.sched[(size_t)p * s.C + c] = x;
+    s.sched[(size_t)c * s.ns + p] = x;
     if (d.gid[x] >= 0) s.cpos[(size_t)(j++) * s.C + c] = (uint16_t)p;
   }
   s.e_x[c] = energy;
-}
-
-// [n][C] -> [C][n] through a 32x32 shared-memory tile (coalesced on both sides)
-__global__ void transpose_u16_kernel(const uint16_t* in, int n, int C, uint16_t* out) {
-  __shared__ uint16_t tile[32][33];
-  int c0 = blockIdx.x * 32, p0 = blockIdx.y * 32;
-  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
-    int p = p0 + dy, c = c0 + threadIdx.x;
-    if (p < n && c < C) tile[dy][threadIdx.x] = in[(size_t)p * C + c];
-  }
-  __syncthreads();
-  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
-    int c = c0 + dy, p = p0 + threadIdx.x;
-    if (p < n && c < C) out[(size_t)c * n + p] = tile[threadIdx.x][dy];
-  }
 }
 
 // ---- API helpers: batch simulate + legality queries ------------------------
@@ -681,9 +681,10 @@ static int chains_alloc(sip_ctx* ctx, sip_kernel* k, const sip_anneal_cfg* cfg, 
   s.unsafe = cfg->unsafe_moves;
   s.hw_safe = cfg->hw_safe;
   s.minfix = cfg->min_fixed_distance;
+  s.ns = (s.n + 7) & ~7;
   size_t C = chains, n = s.n;
-  TRY(dalloc(ctx, &s.sched, n * C));
-  TRY(dalloc(ctx, &s.best, n * C));
+  TRY(dalloc(ctx, &s.sched, (size_t)s.ns * C));
+  TRY(dalloc(ctx, &s.best, (size_t)s.ns * C));
   TRY(dalloc(ctx, &s.cpos, (size_t)std::max(s.k, 1) * C));
   TRY(dalloc(ctx, &s.mt, (size_t)MT_N * C));
   TRY(dalloc(ctx, &s.mti, C));
@@ -725,19 +726,12 @@ static void chains_free(sip_chains* o) {
     if (p) cudaFree(p);
 }
 
-// transpose position-major [n][C] device array into chain-major host [C][n]
-static int fetch_sched(sip_ctx* ctx, const uint16_t* dsrc, int n, int C, uint16_t* host) {
-  uint16_t* tmp = nullptr;
-  TRY(dalloc(ctx, &tmp, (size_t)n * C));
-  dim3 grid((C + 31) / 32, (n + 31) / 32);
-  transpose_u16_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(dsrc, n, C, tmp);
-  int rc = SIP_OK;
-  if (cudaGetLastError() != cudaSuccess) rc = fail(ctx, SIP_E_CUDA, "transpose launch failed");
-  if (rc == SIP_OK) rc = d2h(ctx, host, tmp, (size_t)n * C);
-  if (rc == SIP_OK && cudaStreamSynchronize(ctx->stream) != cudaSuccess)
-    rc = fail(ctx, SIP_E_CUDA, "schedule fetch failed");
-  cudaFree(tmp);
-  return rc;
+// chain-major device rows (pitch ns) -> dense host [C][n]
+static int fetch_sched(sip_ctx* ctx, const uint16_t* dsrc, int n, int ns, int C, uint16_t* host) {
+  SIP_CUDA(ctx, cudaMemcpy2DAsync(host, sizeof(uint16_t) * n, dsrc, sizeof(uint16_t) * ns,
+                                  sizeof(uint16_t) * n, (size_t)C, cudaMemcpyDeviceToHost, ctx->stream));
+  SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return SIP_OK;
 }
 
 static int chains_fetch(sip_chains* o, sip_record* history, uint16_t* best, uint16_t* current,
@@ -746,8 +740,8 @@ static int chains_fetch(sip_chains* o, sip_record* history, uint16_t* best, uint
   Chains& s = o->s;
   size_t C = s.C;
   if (history) TRY(d2h(ctx, history, s.hist, C * s.budget));
-  if (best) TRY(fetch_sched(ctx, s.best, s.n, s.C, best));
-  if (current) TRY(fetch_sched(ctx, s.sched, s.n, s.C, current));
+  if (best) TRY(fetch_sched(ctx, s.best, s.n, s.ns, s.C, best));
+  if (current) TRY(fetch_sched(ctx, s.sched, s.n, s.ns, s.C, current));
   if (summary) {
     std::vector<double> t0(C), ex(C), eb(C);
     std::vector<int32_t> bi(C), am(C);
@@ -982,6 +976,7 @@ int sip_anneal_ex(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds
     TRY(dalloc(ctx, &k->d_base, MT_N));
     TRY(h2d(ctx, k->d_base, mt_base_host().data(), MT_N));
   }
+  o.s.record_hist = history != nullptr;
   o.s.start = nullptr;
   if (start) {
     if (!o.d_start) TRY(dalloc(ctx, &o.d_start, (size_t)o.s.n));
@@ -1008,8 +1003,8 @@ int sip_anneal_ex(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds
       if (sum[c].best_energy < sum[w].best_energy ||
           (sum[c].best_energy == sum[w].best_energy && seeds[c] < seeds[w]))
         w = c;
-    SIP_CUDA(ctx, cudaMemcpy2DAsync(champion, sizeof(uint16_t), o.s.best + w, sizeof(uint16_t) * chains,
-                                    sizeof(uint16_t), (size_t)o.s.n, cudaMemcpyDeviceToHost, ctx->stream));
+    SIP_CUDA(ctx, cudaMemcpyAsync(champion, o.s.best + (size_t)w * o.s.ns, sizeof(uint16_t) * o.s.n,
+                                  cudaMemcpyDeviceToHost, ctx->stream));
     SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     if (champion_chain) *champion_chain = w;
   }

@@ -90,15 +90,10 @@ class HardwareSearch:
             return
         import torch
 
-        dev = torch.device("cuda", self.be.device)
-        mine = torch.tensor([e, float(seed), float(self.rank)], dtype=torch.float64, device=dev)
-        allv = [torch.zeros_like(mine) for _ in range(self.world)]
-        self.dist.all_gather(allv, mine)
-        rows = sorted((float(v[0]), float(v[1]), int(v[2])) for v in allv)
-        be, bs, owner = rows[0]
-        buf = torch.as_tensor(sched.astype(np.int32), device=dev)
-        self.dist.broadcast(buf, src=owner)
-        self.chains.adopt(buf.cpu().numpy().astype(np.uint16), be, be * self.t0)
+        from .parallel import exchange_best
+
+        be, _, _, sched = exchange_best(self.dist, e, seed, sched, torch.device("cuda", self.be.device))
+        self.chains.adopt(sched, be, be * self.t0)
 
     def result(self):
         e, seed, sched, hist, summ = self.local_best()

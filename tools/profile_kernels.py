@@ -1,0 +1,30 @@
+"""Launch each hot kernel a few times for ncu captures (never used for timing)."""
+import sys
+sys.path.insert(0, '.')
+import numpy as np
+import torch
+which = sys.argv[1]
+if which == "gemm":
+    from paper_2403_16863_b200.targets import GemmTarget
+    from paper_2403_16863_b200.evaluator import B200Backend
+    be = B200Backend(GemmTarget(M=4096, N=4096, K=4096).allocate())
+    for _ in range(3):
+        be.run_perm(None)
+elif which == "engine":
+    from bench import decoded_listing
+    from paper_2403_16863_b200 import AnnealConfig
+    from paper_2403_16863_b200.engine import get_context
+    from paper_2403_16863_b200.machine import MachineConfig
+    from paper_2403_16863_b200.tables import KernelTables
+    L = decoded_listing()
+    dk = get_context().kernel(KernelTables.build(L.kernel, MachineConfig()))
+    temps = AnnealConfig().temperatures()
+    for r in range(2):
+        dk.anneal_epoch(np.arange(32768) + r * 32768, temps, with_history=False)
+elif which == "verify":
+    from paper_2403_16863_b200.verify import Verifier
+    v = Verifier("gemm")
+    ident = np.arange(v.module.n, dtype=np.uint16)
+    v.run(ident, 3 * v.batch)
+torch.cuda.synchronize()
+print("done", which)
