@@ -23,6 +23,9 @@ NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 
 LIB_SOURCES = ["context.cu", "engine.cu", "evaluator.cu", "verify.cu", "targets_launch.cu"]
 CUBINS = {"gemm_lrelu": "gemm_lrelu.cu", "attn_fwd": "attn_fwd.cu", "canary": "canary.cu"}
+# build-time variants for descriptor probes, e.g. {"attn_fwd_vswap": ("attn_fwd.cu", ["-DSIP_VDESC_SWAP"])}
+# (the swapped MN-major LBO/SBO encoding was measured wrong on a B200: max err 0.077 vs 4e-5)
+CUBIN_VARIANTS: dict = {}
 
 
 def _run(cmd, cwd=None) -> None:
@@ -68,6 +71,12 @@ def build_cubins(force: bool = False) -> dict:
         deps = [s] + list(TARGETS.glob("*.cuh"))
         if force or _stale(cub, deps):
             _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-cubin", "-o", str(cub), str(s)])
+        out[name] = cub
+    for name, (src, flags) in CUBIN_VARIANTS.items():
+        s = TARGETS / src
+        cub = TARGETS / f"{name}.cubin"
+        if force or _stale(cub, [s] + list(TARGETS.glob("*.cuh"))):
+            _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-cubin", *flags, "-o", str(cub), str(s)])
         out[name] = cub
     return out
 

@@ -74,14 +74,13 @@ int sip_target_attn_launch(sip_ctx* ctx, const void* Q, const void* K, const voi
     return sip::fail(ctx, SIP_E_ARG, "attention target needs D == 128 and S % 128 == 0");
   uint8_t* p = static_cast<uint8_t*>(params);
   std::memset(p, 0, kAttnParamBytes);
-  // [B*H][S][D] viewed as 4-D (64-col half, S, 2 halves of D, B*H) for SWIZZLE_128B boxes of 64 x rows
-  cuuint64_t dims[4] = {64, (cuuint64_t)S, 2, (cuuint64_t)B * H};
-  cuuint64_t strides[3] = {(cuuint64_t)D * 2, 64 * 2, (cuuint64_t)S * D * 2};
-  cuuint32_t box_q[4] = {64, 128, 2, 1};
-  cuuint32_t box_kv[4] = {64, 128, 2, 1};
-  int rc = encode(ctx, reinterpret_cast<CUtensorMap*>(p), Q, 4, dims, strides, box_q);
-  if (rc == SIP_OK) rc = encode(ctx, reinterpret_cast<CUtensorMap*>(p + 128), K, 4, dims, strides, box_kv);
-  if (rc == SIP_OK) rc = encode(ctx, reinterpret_cast<CUtensorMap*>(p + 256), V, 4, dims, strides, box_kv);
+  // [B*H][S][D]: 3-D maps, 64-column (128-byte, SWIZZLE_128B) boxes of 128 rows
+  cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)S, (cuuint64_t)B * H};
+  cuuint64_t strides[2] = {(cuuint64_t)D * 2, (cuuint64_t)S * D * 2};
+  cuuint32_t box[3] = {64, 128, 1};
+  int rc = encode(ctx, reinterpret_cast<CUtensorMap*>(p), Q, 3, dims, strides, box);
+  if (rc == SIP_OK) rc = encode(ctx, reinterpret_cast<CUtensorMap*>(p + 128), K, 3, dims, strides, box);
+  if (rc == SIP_OK) rc = encode(ctx, reinterpret_cast<CUtensorMap*>(p + 256), V, 3, dims, strides, box);
   if (rc != SIP_OK) return rc;
   std::memcpy(p + 384, &O, 8);
   std::memcpy(p + 392, &B, 4);
@@ -96,7 +95,7 @@ int sip_target_attn_launch(sip_ctx* ctx, const void* Q, const void* K, const voi
   launch->block[0] = 256;
   launch->block[1] = launch->block[2] = 1;
   launch->cluster[0] = launch->cluster[1] = launch->cluster[2] = 1;
-  launch->smem_bytes = 0;  // set by the attention target once it lands
+  launch->smem_bytes = 7 * 128 * 128 * 2 + 1024 + 256;
   launch->params = params;
   launch->param_offsets = kAttnOffsets;
   launch->nparams = 9;

@@ -103,3 +103,45 @@ def test_hardware_search_end_to_end():
     assert rep.baseline > 0 and rep.best is not None
     be.run_perm(schedule_perm(rep.best.state.best))
     assert torch.equal(tgt.output, base_out)
+
+
+@pytest.mark.parametrize("shape", [(1, 2, 512), (2, 3, 1024)])
+def test_attention_matches_torch(shape):
+    from paper_2403_16863_b200.attention import AttnTarget
+
+    B, H, S = shape
+    tgt = AttnTarget(B=B, H=H, S=S).allocate()
+    be = B200Backend(tgt)
+    be.run_perm(None)
+    torch.cuda.synchronize()
+    ref = tgt.reference_output()
+    err = (tgt.output.float() - ref).abs()
+    assert bool((err <= 2e-3 + 1e-2 * ref.abs()).all()), f"max err {err.max().item()}"
+
+
+def test_attention_listing_and_verifier():
+    from paper_2403_16863_b200 import candidates
+    from paper_2403_16863_b200.verify import Verifier
+
+    ver = Verifier("attn", batch=64)
+    L = render_listing(*ver.target.cubin())
+    names = {ins.base_mnemonic for ins in L.kernel.schedule}
+    assert {"UTCHMMA", "UTMALDG", "LDTM", "STG", "MUFU"} <= names
+    assert len(candidates(L.kernel)) >= 8
+    res = ver.run(np.arange(L.n, dtype=np.uint16), 128)
+    assert res.ok and res.bitdiff_elems == 0 and res.samples == 128
+
+
+def test_gemm_verifier_detects_a_broken_schedule():
+    """A schedule that breaks the epilogue (store before its data) must fail verification."""
+    from paper_2403_16863_b200.verify import Verifier
+
+    ver = Verifier("gemm", batch=16)
+    L = render_listing(*ver.target.cubin())
+    names = [ins.base_mnemonic for ins in L.kernel.schedule]
+    s = names.index("STG")
+    f = max(i for i in range(s) if names[i] == "F2FP")  # last pack feeding the first stores
+    perm = np.arange(L.n, dtype=np.uint16)
+    perm[f], perm[s] = perm[s], perm[f]
+    res = ver.run(perm, 32)
+    assert not res.ok and res.first_fail_sample == 0
