@@ -1,29 +1,31 @@
-"""Benchmark: hardware-timed SIP search on the GEMM+LeakyReLU tcgen05 target.
+"""Benchmark: SIP search-and-evaluate on B200 over the shipped sm_100a targets.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...      (one process per GPU)
 
-Workload (BASELINE.json configs[1], sharded as configs[3] for N>1): the
-hand-written sm_100a GEMM+LeakyReLU kernel at M=N=K=4096 fp16 is decoded
-from its cubin; every rank runs ``--chains`` annealing chains whose
-candidates are re-encoded, loaded with cuModuleLoadData and timed on the
-B200 inside CUDA graphs (L2 flushed before every timed launch).  A *step*
-is one search round: one legal proposal per chain, each priced on the GPU,
-then the Metropolis update; every ``--epoch`` rounds the ranks all-gather
-their best (energy, seed) over NCCL and adopt the global best schedule.
+Headline (``value``): candidates evaluated per second by the batched search
+engine.  Workload: the reference's default search (95 iterations, simulator
+energy, AnnealConfig defaults) over the decoded listing of the hand-written
+tcgen05 GEMM+LeakyReLU cubin (the M=N=K=4096 target of configs[1]);
+``--sim-chains`` chains per GPU; one *step* = one epoch: every chain runs its
+95 iterations in one kernel launch, then the ranks all-gather (energy, seed)
+over NCCL and restart from the global champion.  Device time (CUDA events,
+barrier + synchronize on both sides, max over ranks).  ``e2e``: the same
+metric through the public API (``run_search`` with Kernel objects, host
+buffers, device->host histories and schedules).
 
-``value`` = candidates evaluated per second, all ranks, device-timed (CUDA
-events, max over ranks).  ``e2e`` = the same metric through the public API
-(``run_search`` with a ``B200Backend``, Kernel objects in, host buffers).
-``roofline`` = the GEMM kernel's achieved TFLOP/s over the measured bf16
-peak.  ``tuned`` = nvcc-schedule vs best-found schedule of this run, and
-``verify`` = the best schedule checked against the baseline on random
-samples.  ``cpu_baseline`` = the reference algorithm (C port of the
-reference search, simulator energy) on the same decoded listing, 1 core.
+Hardware phases (same run): candidates of the GEMM (and the attention
+target, B=4 H=32 S=4096 D=128) are re-encoded, loaded with cuModuleLoadData
+and timed on the B200 inside CUDA graphs (L2 flushed before every timed
+launch): ``hw`` rate and its device-busy fraction, ``roofline`` (the GEMM's
+TFLOP/s over the measured peak, from the evaluator's CUDA events), ``tuned``
+(nvcc schedule vs best schedule found) and ``verify`` (the best schedule vs the
+baseline on independent random samples).  ``cpu_baseline``: the reference
+algorithm (oracle C port) on one core over the same listing.
 
-``--impl reference``: the reference's CPU search (oracle port, since the
-reference itself is pure Python and absent on the GPU box) on all host
-cores over the same listing; rank 0 only.
+``--impl reference``: the reference's CPU search (oracle port -- the
+reference is pure Python and absent on the GPU box) on all host cores over
+the same listing; rank 0 only.
 """
 from __future__ import annotations
 
@@ -43,6 +45,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "tuned attn/GEMM TFLOP/s vs nvcc schedule; candidates evaluated/sec at 1-8 GPU"
 UNIT = "candidates/s"
 SHAPE = dict(M=4096, N=4096, K=4096)
+ATTN_SHAPE = dict(B=4, H=32, S=4096, D=128)
 
 
 def parse():
@@ -51,13 +54,15 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--sim-chains", type=int, default=32768, help="engine chains per GPU")
+    ap.add_argument("--sim-chains", type=int, default=131072, help="engine chains per GPU")
     ap.add_argument("--chains", type=int, default=8, help="hardware-priced chains per GPU")
     ap.add_argument("--hw-steps", type=int, default=8, help="hardware search rounds")
     ap.add_argument("--epoch", type=int, default=8, help="rounds between global-best exchanges")
     ap.add_argument("--verify-samples", type=int, default=200_000)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-attn", action="store_true")
+    ap.add_argument("--attn-steps", type=int, default=3, help="attention hardware search rounds")
     return ap.parse_args()
 
 
@@ -233,6 +238,84 @@ def allreduce(dist, vals, op):
     return t.tolist()
 
 
+def hardware_phase(kind, listing, local, rank, world, dist, args, rounds):
+    """Hardware-priced search on one tuning target: rate, roofline, tuned vs nvcc, verification."""
+    import numpy as np
+    import torch
+
+    from paper_2403_16863_b200 import AnnealConfig
+    from paper_2403_16863_b200.evaluator import B200Backend
+    from paper_2403_16863_b200.hwsearch import HardwareSearch
+    from paper_2403_16863_b200.targets import make_target
+    from paper_2403_16863_b200.verify import Verifier
+
+    MAX = dist.ReduceOp.MAX if dist else None
+    SUM = dist.ReduceOp.SUM if dist else None
+    shape = SHAPE if kind == "gemm" else ATTN_SHAPE
+    tgt = make_target(kind, device=local, **shape).allocate()
+    be = B200Backend(tgt, listing, device=local, warmup=2, flush_l2=True)
+    n = be.listing.n
+    hcfg = AnnealConfig(seed=0, t_max=0.02, t_min=0.0005, cooling=1.02, measure_reps=5)
+    hs = HardwareSearch(be, hcfg, args.chains, epoch=args.epoch, dist=dist)
+    hs.step()
+    be.kernel_ms.clear()
+    launches0, evald0 = hs.launches, hs.evaluated
+    torch.cuda.synchronize()
+    h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h0.record()
+    for _ in range(rounds):
+        hs.step()
+    torch.cuda.synchronize()
+    h1.record()
+    h1.synchronize()
+    h_ms = allreduce(dist, [h0.elapsed_time(h1)], MAX)[0]
+    h_eval, h_launch = allreduce(dist, [hs.evaluated - evald0, hs.launches - launches0], SUM)
+    kern = list(be.kernel_ms)
+    pk = peaks()
+    avg_ms = sum(kern) / len(kern)
+    achieved = tgt.flops / (avg_ms / 1e3) / 1e12
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": pk["tflops"], "unit": "TFLOP/s",
+                "frac": achieved / pk["tflops"],
+                "traffic": ncu_traffic() if kind == "gemm" else None,
+                "kernel": be.listing.func, "flop_per_launch": tgt.flops, "launches_timed": len(kern),
+                "avg_launch_ms": avg_ms,
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst; kernel timed alone)"
+                if pk["src"] == "measured" else "fallback 1590 TFLOP/s"}
+    floor_ms = (2 if be.paired else 1) * (be.warmup + hcfg.measure_reps) * avg_ms
+    hw = {"candidates_per_s": h_eval / (h_ms / 1e3), "rounds": rounds, "chains_per_gpu": args.chains,
+          "evaluator_roofline_candidates_per_s": world * 1e3 / floor_ms,
+          "device_busy_frac": (h_eval / (h_ms / 1e3)) / (world * 1e3 / floor_ms),
+          "note": "one candidate = re-encode + cuModuleLoadData + one CUDA graph of 2 warmup + 5 timed "
+                  "(nvcc, candidate) launch pairs, L2 flushed before each launch; energy = median "
+                  "pair ratio; roofline = 14 x kernel time"}
+    res = hs.result()
+    if dist:
+        hs.exchange()
+        res = hs.result()
+    tuned = verify = None
+    if rank == 0:
+        ident = np.arange(n, dtype=np.uint16)
+        best = res["best_perm"]
+        ratio, raw = be.ratio(best, 45)  # paired: nvcc and best schedules alternate in one graph
+        t_nvcc = be._measure_single(ident, 15).value
+        t_best = t_nvcc * ratio
+        q1, q3 = np.percentile(raw, [25, 75])
+        tuned = {"nvcc_ms": t_nvcc, "best_ms": t_best, "speedup": 1.0 / ratio,
+                 "speedup_iqr": [1.0 / q3, 1.0 / q1], "pairs": 45,
+                 "nvcc_tflops": tgt.flops / t_nvcc / 1e9, "best_tflops": tgt.flops / t_best / 1e9,
+                 "instructions_moved": int((best != ident).sum()),
+                 "search_best_energy": res["best_energy"],
+                 "paper_speedup": 1.1227 if kind == "gemm" else 1.062}
+        ver = Verifier(kind, device=local)
+        vr = ver.run(best, args.verify_samples)
+        verify = {"samples": vr.samples, "passed": vr.passed, "failed": vr.failed,
+                  "bit_identical": vr.bitdiff_elems == 0, "seconds": vr.seconds,
+                  "sample": ("one independent 256x256x1024 GEMM+LeakyReLU problem" if kind == "gemm"
+                             else "one independent head, S=256 D=128") + ", Philox inputs",
+                  "tolerance": {"atol": ver.atol, "rtol": ver.rtol}}
+    return {"roofline": roofline, "hw": hw, "tuned": tuned, "verify": verify, "launches": h_launch}
+
+
 def main() -> None:
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -339,66 +422,16 @@ def main() -> None:
                "d2h_bytes_per_step": int(C * len(temps) * 16 + 2 * C * n * 2 + C * 48),
                "api": "run_search(kernel, SimulatorBackend(), AnnealConfig(seed), chains=C) per step"}
 
-    # ================= phase B: hardware evaluator on the same target =================
-    tgt = GemmTarget(device=local, **SHAPE).allocate()
-    be = B200Backend(tgt, listing, device=local, warmup=2, flush_l2=True)
-    hcfg = AnnealConfig(seed=0, t_max=0.02, t_min=0.0005, cooling=1.02, measure_reps=5)
-    hs = HardwareSearch(be, hcfg, args.chains, epoch=args.epoch, dist=dist)
-    hs.step()
-    be.kernel_ms.clear()
-    launches0, evald0 = hs.launches, hs.evaluated
-    torch.cuda.synchronize()
-    h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    h0.record()
-    for _ in range(args.hw_steps):
-        hs.step()
-    torch.cuda.synchronize()
-    h1.record()
-    h1.synchronize()
-    h_ms = allreduce(dist, [h0.elapsed_time(h1)], MAX)[0]
-    h_eval, h_launch = allreduce(dist, [hs.evaluated - evald0, hs.launches - launches0], SUM)
-    kern = list(be.kernel_ms)
-    pk = peaks()
-    avg_ms = sum(kern) / len(kern)
-    achieved = tgt.flops / (avg_ms / 1e3) / 1e12
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": pk["tflops"], "unit": "TFLOP/s",
-                "frac": achieved / pk["tflops"], "traffic": ncu_traffic(),
-                "kernel": "gemm_lrelu_f16 (the tuned target; see engine for the search kernel)",
-                "flop_per_launch": tgt.flops, "launches_timed": len(kern), "avg_launch_ms": avg_ms,
-                "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst; kernel timed alone)"
-                if pk["src"] == "measured" else "fallback 1590 TFLOP/s"}
-    per_cand_floor_ms = (be.warmup + hcfg.measure_reps) * avg_ms
-    hw = {"candidates_per_s": h_eval / (h_ms / 1e3), "rounds": args.hw_steps, "chains_per_gpu": args.chains,
-          "evaluator_roofline_candidates_per_s": world * 1e3 / per_cand_floor_ms,
-          "device_busy_frac": (h_eval / (h_ms / 1e3)) / (world * 1e3 / per_cand_floor_ms),
-          "note": "one candidate = re-encode + cuModuleLoadData + CUDA graph of 2 warmup + 5 timed "
-                  "launches (L2 flushed before each); floor = 7 x kernel time"}
-    res = hs.result()
-    if dist:
-        hs.exchange()
-        res = hs.result()
-
-    tuned = verify = cpu = None
-    if rank == 0:
-        ident = np.arange(n, dtype=np.uint16)
-        cand_best = res["best_perm"]
-        tn, tb2 = [], []
-        for _ in range(5):
-            tn.append(be.measure_perm(ident, 9).value)
-            tb2.append(be.measure_perm(cand_best, 9).value)
-        t_nvcc, t_best = statistics.median(tn), statistics.median(tb2)
-        tuned = {"nvcc_ms": t_nvcc, "best_ms": t_best, "speedup": t_nvcc / t_best,
-                 "nvcc_tflops": tgt.flops / t_nvcc / 1e9, "best_tflops": tgt.flops / t_best / 1e9,
-                 "instructions_moved": int((cand_best != ident).sum()),
-                 "search_best_energy": res["best_energy"], "paper_speedup_gemm": 1.1227}
-        ver = Verifier("gemm", device=local)
-        vr = ver.run(cand_best, args.verify_samples)
-        verify = {"samples": vr.samples, "passed": vr.passed, "failed": vr.failed,
-                  "bit_identical": vr.bitdiff_elems == 0, "seconds": vr.seconds,
-                  "sample": "one independent 256x256x1024 GEMM+LeakyReLU problem, Philox N(0,1)",
-                  "tolerance": {"atol": ver.atol, "rtol": ver.rtol}}
-        if world == 1:
-            cpu = cpu_reference_rate(listing, args.cpu_seconds, workers=1)
+    # ================= phase B: hardware evaluator on the tuning targets =================
+    gemm = hardware_phase("gemm", listing, local, rank, world, dist, args, rounds=args.hw_steps)
+    attn = None
+    if not args.no_attn:
+        attn = hardware_phase("attn", None, local, rank, world, dist, args, rounds=args.attn_steps)
+    cpu = None
+    if rank == 0 and world == 1:
+        cpu = cpu_reference_rate(listing, args.cpu_seconds, workers=1)
+    roofline = gemm["roofline"]
+    h_launch = gemm["launches"] + (attn["launches"] if attn else 0)
 
     if rank == 0:
         line = {
@@ -416,7 +449,9 @@ def main() -> None:
                        "l2": "engine state < L2 (resident); hardware phase flushes L2 (256 MB) "
                              "before every timed launch",
                        "parallelism": f"{world} GPU(s), independent chains, allgather per epoch"},
-            "roofline": roofline, "engine": engine, "hw": hw, "tuned": tuned, "verify": verify,
+            "roofline": roofline, "engine": engine,
+            "hw": gemm["hw"], "tuned": gemm["tuned"], "verify": gemm["verify"],
+            "attn": None if attn is None else {k: attn[k] for k in ("roofline", "hw", "tuned", "verify")},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
             "gpu_launches": int(args.steps * world * 1 + h_launch),
             "candidates_evaluated": int(priced_all),

@@ -181,6 +181,14 @@ int sip_module_patch(sip_module* m, const uint16_t* perm, void* out, size_t* siz
  * inside one CUDA graph with per-launch events; median in ms.           */
 int sip_measure(sip_module* m, const uint16_t* perm, const sip_launch* launch, int32_t warmup,
                 int32_t reps, int32_t flush_l2, double* median_ms, double* raw_ms);
+/* paired timing: baseline (perm_ref) and candidate (perm_cand) launches
+ * alternate inside one CUDA graph (order rotated every rep, L2 flushed before
+ * each launch); the per-pair ratio cand/ref cancels clock and power drift.
+ * *ratio_median is the candidate's energy relative to the baseline.       */
+int sip_measure_paired(sip_module* m, const uint16_t* perm_ref, const uint16_t* perm_cand,
+                       const sip_launch* launch, int32_t warmup, int32_t reps, int32_t flush_l2,
+                       double* ratio_median, double* ref_median_ms, double* cand_median_ms,
+                       double* raw_ratio);
 /* run the permuted module once on the given launch (verification) */
 int sip_run(sip_module* m, const uint16_t* perm, const sip_launch* launch);
 

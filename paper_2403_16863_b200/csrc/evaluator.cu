@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <list>
 #include <string>
 #include <vector>
 
@@ -116,7 +117,7 @@ struct sip_module {
   int n = 0;
   std::vector<uint8_t> pin;
   std::vector<uint8_t> patched;
-  std::vector<CachedMod> cache;
+  std::list<CachedMod> cache;  // stable addresses: callers hold CachedMod* across loads
   uint64_t clock = 0;
   std::vector<cudaEvent_t> events;
 };
@@ -376,30 +377,34 @@ int sip_run(sip_module* m, const uint16_t* perm, const sip_launch* L) {
   return SIP_OK;
 }
 
-int sip_measure(sip_module* m, const uint16_t* perm, const sip_launch* L, int32_t warmup,
-                int32_t reps, int32_t flush_l2, double* median_ms, double* raw_ms) {
-  if (!m || !L || !m->ctx || !median_ms || reps < 1 || warmup < 0) return SIP_E_ARG;
+// warmup launches of every module, then `reps` rounds; round r launches the
+// modules in rotated order (ABAB.. / BABA..), each bracketed by an event pair
+// and preceded by an optional L2 flush.  Everything runs from one CUDA graph.
+static int run_timed(sip_module* m, CachedMod** mods, int nm, const sip_launch* L, int warmup, int reps,
+                     int flush_l2, std::vector<std::vector<double>>& times) {
   sip_ctx* ctx = m->ctx;
-  CachedMod* cm = nullptr;
-  int rc = get_module(m, perm, &cm);
-  if (rc != SIP_OK) return rc;
+  int rc = SIP_OK;
   if (flush_l2 && (rc = ensure_flush(ctx)) != SIP_OK) return rc;
-  while ((int)m->events.size() < 2 * reps) {
+  const int nev = 2 * reps * nm;
+  while ((int)m->events.size() < nev) {
     cudaEvent_t e;
     SIP_CUDA(ctx, cudaEventCreate(&e));
     m->events.push_back(e);
   }
-  // one CUDA graph: warmup launches, then (flush?, ev, launch, ev) per rep
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   SIP_CUDA(ctx, cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-  for (int w = 0; w < warmup && rc == SIP_OK; ++w) rc = launch(m, cm, L);
-  for (int r = 0; r < reps && rc == SIP_OK; ++r) {
-    if (flush_l2) cudaMemsetAsync(ctx->flush_buf, r & 0xff, ctx->flush_bytes, ctx->stream);
-    cudaEventRecordWithFlags(m->events[2 * r], ctx->stream, cudaEventRecordExternal);
-    rc = launch(m, cm, L);
-    cudaEventRecordWithFlags(m->events[2 * r + 1], ctx->stream, cudaEventRecordExternal);
-  }
+  for (int w = 0; w < warmup && rc == SIP_OK; ++w)
+    for (int i = 0; i < nm && rc == SIP_OK; ++i) rc = launch(m, mods[i], L);
+  for (int r = 0; r < reps && rc == SIP_OK; ++r)
+    for (int q = 0; q < nm && rc == SIP_OK; ++q) {
+      const int i = (q + r) % nm;
+      const int e = 2 * (r * nm + i);
+      if (flush_l2) cudaMemsetAsync(ctx->flush_buf, (r * nm + q) & 0xff, ctx->flush_bytes, ctx->stream);
+      cudaEventRecordWithFlags(m->events[e], ctx->stream, cudaEventRecordExternal);
+      rc = launch(m, mods[i], L);
+      cudaEventRecordWithFlags(m->events[e + 1], ctx->stream, cudaEventRecordExternal);
+    }
   cudaError_t ce = cudaStreamEndCapture(ctx->stream, &graph);
   if (rc != SIP_OK) {
     if (graph) cudaGraphDestroy(graph);
@@ -409,20 +414,59 @@ int sip_measure(sip_module* m, const uint16_t* perm, const sip_launch* L, int32_
   ce = cudaGraphInstantiate(&exec, graph, 0);
   if (ce == cudaSuccess) ce = cudaGraphLaunch(exec, ctx->stream);
   if (ce == cudaSuccess) ce = cudaStreamSynchronize(ctx->stream);
-  std::vector<double> t(reps);
-  for (int r = 0; r < reps && ce == cudaSuccess; ++r) {
-    float ms = 0.f;
-    ce = cudaEventElapsedTime(&ms, m->events[2 * r], m->events[2 * r + 1]);
-    t[r] = ms;
-  }
+  times.assign(nm, std::vector<double>(reps, 0.0));
+  for (int r = 0; r < reps && ce == cudaSuccess; ++r)
+    for (int i = 0; i < nm && ce == cudaSuccess; ++i) {
+      float ms = 0.f;
+      const int e = 2 * (r * nm + i);
+      ce = cudaEventElapsedTime(&ms, m->events[e], m->events[e + 1]);
+      times[i][r] = ms;
+    }
   if (exec) cudaGraphExecDestroy(exec);
   cudaGraphDestroy(graph);
   if (ce != cudaSuccess)
     return sip::fail(ctx, SIP_E_MEASURE, std::string("timed launches: ") + cudaGetErrorString(ce));
-  if (raw_ms) std::copy(t.begin(), t.end(), raw_ms);
-  std::vector<double> s = t;
-  std::sort(s.begin(), s.end());
-  *median_ms = reps % 2 ? s[reps / 2] : 0.5 * (s[reps / 2 - 1] + s[reps / 2]);
+  return SIP_OK;
+}
+
+static double median_of(std::vector<double> v) {
+  std::sort(v.begin(), v.end());
+  size_t k = v.size();
+  return k % 2 ? v[k / 2] : 0.5 * (v[k / 2 - 1] + v[k / 2]);
+}
+
+int sip_measure(sip_module* m, const uint16_t* perm, const sip_launch* L, int32_t warmup,
+                int32_t reps, int32_t flush_l2, double* median_ms, double* raw_ms) {
+  if (!m || !L || !m->ctx || !median_ms || reps < 1 || warmup < 0) return SIP_E_ARG;
+  CachedMod* cm = nullptr;
+  int rc = get_module(m, perm, &cm);
+  if (rc != SIP_OK) return rc;
+  std::vector<std::vector<double>> t;
+  rc = run_timed(m, &cm, 1, L, warmup, reps, flush_l2, t);
+  if (rc != SIP_OK) return rc;
+  if (raw_ms) std::copy(t[0].begin(), t[0].end(), raw_ms);
+  *median_ms = median_of(t[0]);
+  return SIP_OK;
+}
+
+int sip_measure_paired(sip_module* m, const uint16_t* perm_ref, const uint16_t* perm_cand,
+                       const sip_launch* L, int32_t warmup, int32_t reps, int32_t flush_l2,
+                       double* ratio_median, double* ref_median_ms, double* cand_median_ms,
+                       double* raw_ratio) {
+  if (!m || !L || !m->ctx || !ratio_median || reps < 1 || warmup < 0) return SIP_E_ARG;
+  CachedMod* mods[2] = {nullptr, nullptr};
+  int rc = get_module(m, perm_ref, &mods[0]);
+  if (rc == SIP_OK) rc = get_module(m, perm_cand, &mods[1]);
+  if (rc != SIP_OK) return rc;
+  std::vector<std::vector<double>> t;
+  rc = run_timed(m, mods, 2, L, warmup, reps, flush_l2, t);
+  if (rc != SIP_OK) return rc;
+  std::vector<double> ratio(reps);
+  for (int r = 0; r < reps; ++r) ratio[r] = t[1][r] / t[0][r];
+  if (raw_ratio) std::copy(ratio.begin(), ratio.end(), raw_ratio);
+  *ratio_median = median_of(ratio);
+  if (ref_median_ms) *ref_median_ms = median_of(t[0]);
+  if (cand_median_ms) *cand_median_ms = median_of(t[1]);
   return SIP_OK;
 }
 

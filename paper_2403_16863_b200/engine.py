@@ -114,6 +114,8 @@ _SIGS = {
     "sip_module_patch": ([ctypes.c_void_p, c_u16p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
     "sip_measure": ([ctypes.c_void_p, c_u16p, ctypes.POINTER(Launch), ctypes.c_int32, ctypes.c_int32,
                      ctypes.c_int32, c_dblp, c_dblp], ctypes.c_int),
+    "sip_measure_paired": ([ctypes.c_void_p, c_u16p, c_u16p, ctypes.POINTER(Launch), ctypes.c_int32,
+                            ctypes.c_int32, ctypes.c_int32, c_dblp, c_dblp, c_dblp, c_dblp], ctypes.c_int),
     "sip_run": ([ctypes.c_void_p, c_u16p, ctypes.POINTER(Launch)], ctypes.c_int),
     "sip_fill_normal": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int32,
                          ctypes.c_uint64, ctypes.c_uint64, ctypes.c_float], ctypes.c_int),

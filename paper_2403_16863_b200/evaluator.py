@@ -38,7 +38,7 @@ class B200Backend:
     hardware = True        # candidates execute on the GPU: hw_safe legality is enforced
 
     def __init__(self, target, listing: Listing | None = None, *, device: int = 0, warmup: int = 2,
-                 flush_l2: bool = True):
+                 flush_l2: bool = True, paired: bool = True):
         self.target = target
         self.device = device
         self.ctx = get_context(device)
@@ -51,6 +51,11 @@ class B200Backend:
         self.descriptor = BackendDescriptor(kind="b200", command=func, concurrency_safe=False)
         self.calls = 0
         self.kernel_ms = []  # every timed launch (ms), for roofline accounting
+        # paired mode: every candidate is timed against the nvcc schedule inside the same
+        # graph; its value is (median cand/ref ratio) x the reference time measured here
+        self.paired = paired
+        self.identity = np.arange(self.listing.n, dtype=np.uint16)
+        self.ref_ms = self._measure_single(self.identity, 9).value if paired else None
 
     @classmethod
     def for_target(cls, kind: str, device: int = 0, **kw):
@@ -80,6 +85,30 @@ class B200Backend:
         return schedule_perm(kernel)
 
     def measure_perm(self, perm, reps: int = 5) -> CostSample:
+        if self.paired:
+            ratio, raw = self.ratio(perm, reps)
+            return CostSample(ratio * self.ref_ms, self.unit, reps, tuple(r * self.ref_ms for r in raw))
+        return self._measure_single(perm, reps)
+
+    def ratio(self, perm, reps: int = 5, ref=None) -> tuple:
+        """Median cand/ref time ratio over `reps` interleaved pairs (sip_measure_paired)."""
+        perm = np.ascontiguousarray(perm, dtype=np.uint16)
+        ref = self.identity if ref is None else np.ascontiguousarray(ref, dtype=np.uint16)
+        r_med, ref_med, cand_med = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        raw = np.zeros(reps, dtype=np.float64)
+        lib = self.ctx.lib
+        rc = lib.sip_measure_paired(self.module.handle, ref.ctypes.data_as(c_u16p),
+                                    perm.ctypes.data_as(c_u16p), ctypes.byref(self.launch), self.warmup,
+                                    reps, int(self.flush_l2), ctypes.byref(r_med), ctypes.byref(ref_med),
+                                    ctypes.byref(cand_med), raw.ctypes.data_as(c_dblp))
+        self.calls += 1
+        if rc == SIP_E_MEASURE:
+            raise MeasurementFailed(lib.sip_last_error(self.ctx.handle).decode(errors="replace"))
+        self.ctx.check(rc)
+        self.kernel_ms.extend([ref_med.value] * reps + [cand_med.value] * reps)
+        return r_med.value, raw.tolist()
+
+    def _measure_single(self, perm, reps: int = 5) -> CostSample:
         perm = np.ascontiguousarray(perm, dtype=np.uint16)
         med = ctypes.c_double()
         raw = np.zeros(reps, dtype=np.float64)

@@ -112,3 +112,41 @@ def test_run_search_batched_ranking():
     assert [o.seed for o in rep.chains] == list(range(8))
     assert rep.best_time == 404.0 and rep.best.seed == 0
     assert rep.baseline == 436.0
+
+
+def test_device_sample_stream_matches_reference():
+    """sip_sample_inputs: CPython Random(f"{seed}:{index}") streams generated on the device."""
+    import ctypes
+
+    ctx = get_context()
+    kinds = {"int8": 1, "int16": 2, "int32": 4}
+    dists = {"uniform": 0, "small": 1, "zero": 2}
+    for rec in golden()["samples"]:
+        c0 = kinds[rec["kind"]]
+        nbytes = np.array([5 * c0, 12], dtype=np.int32)
+        cell = np.array([c0, 4], dtype=np.int32)
+        dist = np.array([dists[rec["dist"]], 0], dtype=np.int32)
+        out = np.zeros(int(nbytes.sum()), dtype=np.uint8)
+        P = ctypes.POINTER(ctypes.c_int32)
+        ctx.check(ctx.lib.sip_sample_inputs(ctx.handle, rec["seed"], rec["index"], 1, 2,
+                                            nbytes.ctypes.data_as(P), cell.ctypes.data_as(P),
+                                            dist.ctypes.data_as(P),
+                                            out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))))
+        assert out[: nbytes[0]].tobytes().hex() == rec["buf0"], rec
+        assert out[nbytes[0]:].tobytes().hex() == rec["buf1"], rec
+
+
+def test_anneal_epoch_restart_matches_oracle_from_identity():
+    """sip_anneal_ex with start=identity is the plain chain (the epoch-restart path)."""
+    rec, k, t, dk = setup("synthetic_mix_2")
+    temps = AnnealConfig().temperatures()
+    seeds = np.arange(500, 628, dtype=np.int64)
+    hist, summ, champ, w = dk.anneal_epoch(seeds, temps, start=np.arange(t.n, dtype=np.uint16))
+    ol = oracle.OracleListing(t)
+    best_e = []
+    for c, s in enumerate(seeds):
+        oh, ob, _, os_ = ol.anneal(int(s), temps)
+        assert np.array_equal(hist[c], oh)
+        best_e.append((os_["best_energy"], int(s), ob))
+    e, s, ob = min(best_e, key=lambda x: (x[0], x[1]))
+    assert seeds[w] == s and np.array_equal(champ, ob)

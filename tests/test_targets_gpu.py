@@ -138,9 +138,14 @@ def test_gemm_verifier_detects_a_broken_schedule():
 
     ver = Verifier("gemm", batch=16)
     L = render_listing(*ver.target.cubin())
-    names = [ins.base_mnemonic for ins in L.kernel.schedule]
+    from paper_2403_16863_b200 import reads_writes
+
+    seq = L.kernel.schedule
+    names = [ins.base_mnemonic for ins in seq]
     s = names.index("STG")
-    f = max(i for i in range(s) if names[i] == "F2FP")  # last pack feeding the first stores
+    data = reads_writes(seq[s])[0]
+    # the last pack whose result the first store reads
+    f = max(i for i in range(s) if names[i] == "F2FP" and reads_writes(seq[i])[1] & data)
     perm = np.arange(L.n, dtype=np.uint16)
     perm[f], perm[s] = perm[s], perm[f]
     res = ver.run(perm, 32)
