@@ -217,6 +217,23 @@ int sip_sample_inputs(sip_ctx* ctx, int64_t seed, int64_t first, int32_t count, 
                       const int32_t* nbytes, const int32_t* cell, const int32_t* dist,
                       uint8_t* out);
 
+/* same stream written to a device buffer [count][sum nbytes] */
+int sip_sample_inputs_device(sip_ctx* ctx, int64_t seed, int64_t first, int32_t count, int32_t nbuf,
+                             const int32_t* nbytes, const int32_t* cell, const int32_t* dist, void* dev_out);
+
+/* ---- GPU interpreter of the reference's integer SASS subset ------------
+ * machine.CompiledKernel.run (machine.py:698-711): one device thread per
+ * sample executes `prog` (64-byte ops compiled by interp.py) on its slice
+ * region + s*stride of the buffers (virtual bases[b], lens[b] bytes at offs[b]).
+ * status[s]: 0 ok, 1 global / 2 shared out of bounds, 3 uninitialised read
+ * (strict), low byte = code, bits 8.. = access size; fault[s] = address.     */
+int sip_vm_exec(sip_ctx* ctx, const void* prog, int32_t nops, int32_t nbuf, const int64_t* bases,
+                const int32_t* lens, const int32_t* offs, void* region, int64_t stride, int32_t count,
+                int32_t shared_bytes, int32_t strict, int32_t* status, int64_t* fault);
+/* first differing cell of bytes [off, off+nbytes) between two regions, per sample (-1 = equal) */
+int sip_vm_cell_diff(sip_ctx* ctx, const void* a, const void* b, int64_t stride, int32_t off, int32_t nbytes,
+                     int32_t cell, int32_t count, int32_t* first_cell);
+
 /* ---- tuning targets (G7/G8): launch descriptors for the shipped cubins -- */
 /* GEMM+LeakyReLU: C[l] = leaky(A[l] (MxK, row-major) * B[l]^T (NxK, row-major)) fp16 */
 int sip_target_gemm_launch(sip_ctx* ctx, const void* A, const void* B, void* C, int32_t M,

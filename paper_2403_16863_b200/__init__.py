@@ -8,10 +8,14 @@ from .anneal import (AnnealConfig, AnnealState, HistoryRecord, InvalidBaseline, 
                      feedback)
 from .backends import (BackendDescriptor, CostSample, ExternalCommandBackend, MeasurementFailed,
                        SimulatorBackend, make_backend)
+from .difftest import (BufferSpec, FailureDetail, TestPlan, TestVerdict, first_failure_index, pass_curve,
+                       run_tests, sample_inputs)
 from .deps import DepEdge, DepGraph, DepKind, build_depgraph, mem_refs, reads_writes, swap_legal
 from .driver import ChainOutcome, SearchReport, run_search
 from .ir import (ControlCode, ControlError, Instruction, InstrClass, Kernel, Operand, OperandKind,
                  classify)
+from .interp import (CompiledKernel, OutOfBoundsAccess, UninitializedRead, UnsupportedInstruction,
+                     interpret)
 from .machine import MachineConfig, SimReport, simulate
 from .perturb import (Action, CandidateSet, Direction, MoveRejected, NoCandidatesError, apply_action,
                       candidates, sample_action)

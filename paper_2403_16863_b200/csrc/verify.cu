@@ -320,27 +320,24 @@ int sip_compare(sip_ctx* ctx, const void* ref, const void* cand, size_t count, i
   return SIP_OK;
 }
 
-int sip_sample_inputs(sip_ctx* ctx, int64_t seed, int64_t first, int32_t count, int32_t nbuf,
-                      const int32_t* nbytes, const int32_t* cell, const int32_t* dist, uint8_t* out) {
-  if (!ctx || count < 0 || nbuf < 0 || (nbuf && (!nbytes || !cell || !dist)) || (count && !out))
-    return SIP_E_ARG;
-  if (count == 0) return SIP_OK;
+static int sample_inputs_impl(sip_ctx* ctx, int64_t seed, int64_t first, int32_t count, int32_t nbuf,
+                              const int32_t* nbytes, const int32_t* cell, const int32_t* dist, uint8_t* d_out,
+                              int64_t* stride_out) {
   int64_t stride = 0;
   for (int k = 0; k < nbuf; ++k) {
     if (nbytes[k] < 0 || cell[k] < 1 || dist[k] < 0 || dist[k] > 2 || nbytes[k] % cell[k])
       return sip::fail(ctx, SIP_E_ARG, "bad buffer spec");
     stride += nbytes[k];
   }
+  *stride_out = stride;
+  if (count == 0) return SIP_OK;
   std::vector<uint32_t> base(sip::MT_N);
   sip::MtRef b{base.data(), 1, 0};
   sip::mt_init_genrand(b, 19650218u);
   uint32_t* d_base = nullptr;
   int32_t* d_spec = nullptr;
-  uint8_t* d_out = nullptr;
-  size_t bytes = (size_t)count * (size_t)(stride ? stride : 1);
   SIP_CUDA(ctx, cudaMallocAsync(&d_base, sizeof(uint32_t) * sip::MT_N, ctx->stream));
   SIP_CUDA(ctx, cudaMallocAsync(&d_spec, sizeof(int32_t) * 3 * (nbuf ? nbuf : 1), ctx->stream));
-  SIP_CUDA(ctx, cudaMallocAsync(&d_out, bytes, ctx->stream));
   SIP_CUDA(ctx, cudaMemcpyAsync(d_base, base.data(), sizeof(uint32_t) * sip::MT_N, cudaMemcpyHostToDevice, ctx->stream));
   if (nbuf) {
     SIP_CUDA(ctx, cudaMemcpyAsync(d_spec, nbytes, sizeof(int32_t) * nbuf, cudaMemcpyHostToDevice, ctx->stream));
@@ -350,10 +347,36 @@ int sip_sample_inputs(sip_ctx* ctx, int64_t seed, int64_t first, int32_t count, 
   sample_inputs_kernel<<<(count + 63) / 64, 64, 0, ctx->stream>>>(d_base, seed, first, count, nbuf, d_spec,
                                                                  d_spec + nbuf, d_spec + 2 * nbuf, stride, d_out);
   SIP_CHECK_LAUNCH(ctx);
-  SIP_CUDA(ctx, cudaMemcpyAsync(out, d_out, (size_t)count * stride, cudaMemcpyDeviceToHost, ctx->stream));
   cudaFreeAsync(d_base, ctx->stream);
   cudaFreeAsync(d_spec, ctx->stream);
+  return SIP_OK;
+}
+
+int sip_sample_inputs(sip_ctx* ctx, int64_t seed, int64_t first, int32_t count, int32_t nbuf,
+                      const int32_t* nbytes, const int32_t* cell, const int32_t* dist, uint8_t* out) {
+  if (!ctx || count < 0 || nbuf < 0 || (nbuf && (!nbytes || !cell || !dist)) || (count && !out))
+    return SIP_E_ARG;
+  int64_t stride = 0;
+  for (int k = 0; k < nbuf; ++k) stride += nbytes[k] > 0 ? nbytes[k] : 0;
+  if (count == 0) return SIP_OK;
+  uint8_t* d_out = nullptr;
+  SIP_CUDA(ctx, cudaMallocAsync(&d_out, (size_t)count * (size_t)(stride ? stride : 1), ctx->stream));
+  int rc = sample_inputs_impl(ctx, seed, first, count, nbuf, nbytes, cell, dist, d_out, &stride);
+  if (rc == SIP_OK && stride)
+    SIP_CUDA(ctx, cudaMemcpyAsync(out, d_out, (size_t)count * stride, cudaMemcpyDeviceToHost, ctx->stream));
   cudaFreeAsync(d_out, ctx->stream);
+  SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return rc;
+}
+
+int sip_sample_inputs_device(sip_ctx* ctx, int64_t seed, int64_t first, int32_t count, int32_t nbuf,
+                             const int32_t* nbytes, const int32_t* cell, const int32_t* dist, void* dev_out) {
+  if (!ctx || count < 0 || nbuf < 0 || (nbuf && (!nbytes || !cell || !dist)) || (count && !dev_out))
+    return SIP_E_ARG;
+  int64_t stride = 0;
+  int rc = sample_inputs_impl(ctx, seed, first, count, nbuf, nbytes, cell, dist, static_cast<uint8_t*>(dev_out),
+                              &stride);
+  if (rc != SIP_OK) return rc;
   SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return SIP_OK;
 }

@@ -124,6 +124,13 @@ _SIGS = {
                      ctypes.POINTER(CmpResult)], ctypes.c_int),
     "sip_sample_inputs": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                            c_i32p, c_i32p, c_i32p, c_u8p], ctypes.c_int),
+    "sip_sample_inputs_device": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+                                  ctypes.c_int32, c_i32p, c_i32p, c_i32p, ctypes.c_void_p], ctypes.c_int),
+    "sip_vm_exec": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, c_i64p, c_i32p, c_i32p,
+                     ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, c_i32p,
+                     c_i64p], ctypes.c_int),
+    "sip_vm_cell_diff": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                          ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, c_i32p], ctypes.c_int),
     "sip_target_gemm_launch": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                 ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                 ctypes.c_float, ctypes.POINTER(Launch), ctypes.c_void_p,
