@@ -12,6 +12,7 @@ from .difftest import (BufferSpec, FailureDetail, TestPlan, TestVerdict, first_f
                        run_tests, sample_inputs)
 from .deps import DepEdge, DepGraph, DepKind, build_depgraph, mem_refs, reads_writes, swap_legal
 from .driver import ChainOutcome, SearchReport, run_search
+from .estimator import ScheduleTuner, as_kernel
 from .ir import (ControlCode, ControlError, Instruction, InstrClass, Kernel, Operand, OperandKind,
                  classify)
 from .interp import (CompiledKernel, OutOfBoundsAccess, UninitializedRead, UnsupportedInstruction,

@@ -1,0 +1,68 @@
+"""Public surface end to end on the GPU: CLI, config, store, estimator (reference
+cli.py / store.py / estimator.py behaviours, incl. the README hide.sass run)."""
+import json
+
+import pytest
+
+from paper_2403_16863_b200 import ScheduleTuner, parse_kernel
+from paper_2403_16863_b200.cli import main
+
+pytestmark = pytest.mark.gpu
+
+HIDE = (
+    "[B------:R-:W-:-:S08] IADD3 R20, RZ, 0x1, RZ ;\n[B------:R-:W-:-:S08] IADD3 R21, RZ, 0x1, RZ ;\n"
+    "[B------:R-:W-:-:S08] IADD3 R22, RZ, 0x1, RZ ;\n[B------:R-:W-:-:S08] IADD3 R23, RZ, 0x1, RZ ;\n"
+    "[B------:R-:W0:-:S01] LDG.E R4, [R2.64] ;\n[B0-----:R-:W-:-:S01] IADD3 R5, R4, 0x1, RZ ;\n"
+)
+
+
+def test_optimize_report_and_store(tmp_path, capsys):
+    f = tmp_path / "hide.sass"
+    f.write_text(HIDE)
+    rc = main(["optimize", str(f), "--store", str(tmp_path / "store")])
+    out = capsys.readouterr().out.splitlines()
+    assert rc == 0
+    assert out[0] == "input: hide  instructions: 6  candidates: 1"
+    assert out[1] == "baseline: 436 cycles"
+    assert out[2] == "chain seed=0: best 404 cycles after 95 iterations, tests skipped"
+    assert out[3] == "best: 404 cycles (seed 0), improvement 7.34%"
+    store_dir = out[4].split(": ", 1)[1]
+    best = (tmp_path / "store" / store_dir.split("/")[-1] / "best.sass").read_text()
+    assert best.splitlines()[0] == "[B------:R-:W0:-:S01] LDG.E R4, [R2.64] ;"
+    manifest = json.loads((tmp_path / "store" / store_dir.split("/")[-1] / "manifest.json").read_text())
+    assert manifest["best"]["time"] == 404.0
+
+
+def test_exit_codes(tmp_path, capsys):
+    alu = tmp_path / "alu.sass"
+    alu.write_text("MOV R0, RZ ;\nMOV R1, RZ ;\n")
+    assert main(["optimize", str(alu)]) == 3
+    bad = tmp_path / "bad.sass"
+    bad.write_text("[B------:R-:W-:-:S99] MOV R0, RZ ;\n")
+    assert main(["optimize", str(bad)]) == 2
+    h = tmp_path / "h.sass"
+    h.write_text(HIDE)
+    assert main(["optimize", str(h), "--backend", "nope"]) == 4
+    assert main(["verify", str(h), str(h)]) == 1
+
+
+def test_simulate_and_diff(tmp_path, capsys):
+    a = tmp_path / "a.sass"
+    a.write_text(HIDE)
+    lines = HIDE.splitlines()
+    b = tmp_path / "b.sass"
+    b.write_text("\n".join([lines[4]] + lines[:4] + [lines[5]]) + "\n")
+    assert main(["simulate", str(a)]) == 0
+    assert json.loads(capsys.readouterr().out)["total_cycles"] == 436
+    assert main(["diff", str(a), str(b)]) == 0
+    moves = json.loads(capsys.readouterr().out)["moves"]
+    assert moves == [{"swap": [3, 4]}, {"swap": [2, 3]}, {"swap": [1, 2]}, {"swap": [0, 1]}]
+
+
+def test_estimator_fit_transform():
+    t = ScheduleTuner(chains=3)
+    out = t.fit_transform(HIDE)
+    assert t.best_time_ == 404.0 and t.n_iterations_ == 285
+    assert parse_kernel(out).schedule[0].base_mnemonic == "LDG"
+    with pytest.raises(ValueError):
+        t.transform("MOV R0, RZ ;\n")
