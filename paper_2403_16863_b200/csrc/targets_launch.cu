@@ -70,8 +70,8 @@ int sip_target_attn_launch(sip_ctx* ctx, const void* Q, const void* K, const voi
                            int32_t H, int32_t S, int32_t D, float scale, sip_launch* launch, void* params,
                            uint32_t params_cap) {
   if (!ctx || !Q || !K || !V || !O || !launch || !params || params_cap < kAttnParamBytes) return SIP_E_ARG;
-  if (B <= 0 || H <= 0 || S <= 0 || D != 128 || S % 128)
-    return sip::fail(ctx, SIP_E_ARG, "attention target needs D == 128 and S % 128 == 0");
+  if (B <= 0 || H <= 0 || S <= 0 || D != 128 || S % 256)
+    return sip::fail(ctx, SIP_E_ARG, "attention target needs D == 128 and S % 256 == 0");
   uint8_t* p = static_cast<uint8_t*>(params);
   std::memset(p, 0, kAttnParamBytes);
   // [B*H][S][D]: 3-D maps, 64-column (128-byte, SWIZZLE_128B) boxes of 128 rows
@@ -89,13 +89,13 @@ int sip_target_attn_launch(sip_ctx* ctx, const void* Q, const void* K, const voi
   std::memcpy(p + 404, &D, 4);
   std::memcpy(p + 408, &scale, 4);
   std::memset(launch, 0, sizeof *launch);
-  launch->grid[0] = (uint32_t)(S / 128);
+  launch->grid[0] = (uint32_t)(S / 256);  // two 128-row query tiles per CTA
   launch->grid[1] = (uint32_t)(B * H);
   launch->grid[2] = 1;
-  launch->block[0] = 256;
+  launch->block[0] = 384;
   launch->block[1] = launch->block[2] = 1;
   launch->cluster[0] = launch->cluster[1] = launch->cluster[2] = 1;
-  launch->smem_bytes = 7 * 128 * 128 * 2 + 1024 + 256;
+  launch->smem_bytes = 6 * 128 * 128 * 2 + 1024 + 256;
   launch->params = params;
   launch->param_offsets = kAttnOffsets;
   launch->nparams = 9;

@@ -1,0 +1,21 @@
+"""A/B/C of attention cubin variants in one process (same inputs, same launch)."""
+import sys
+sys.path.insert(0, '.')
+import torch
+from paper_2403_16863_b200.attention import AttnTarget
+from paper_2403_16863_b200.cubin import Module, schedule_perm
+from paper_2403_16863_b200.engine import get_context
+import ctypes, numpy as np
+variants = {"current": "paper_2403_16863_b200/targets/attn_fwd.cubin"}
+for a in sys.argv[1:]:
+    variants[a.split("/")[-1]] = a
+tgt = AttnTarget(B=4, H=32, S=4096).allocate()
+ctx = get_context()
+mods = {k: Module(open(v, 'rb').read(), "attn_fwd_f16", ctx=ctx) for k, v in variants.items()}
+for rnd in range(3):
+    for k, m in mods.items():
+        lp, params = tgt.launch()
+        med = ctypes.c_double(); raw = np.zeros(10)
+        ctx.check(ctx.lib.sip_measure(m.handle, None, ctypes.byref(lp), 2, 10, 0, ctypes.byref(med),
+                                      raw.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        print(f"{k:20s} {med.value*1e3:8.1f} us  {tgt.flops/med.value/1e9:7.1f} TFLOP/s", flush=True)

@@ -6,7 +6,7 @@ from paper_2403_16863_b200.attention import AttnTarget
 from paper_2403_16863_b200.evaluator import B200Backend
 from paper_2403_16863_b200.cubin import schedule_perm
 
-for cub in ["attn_fwd.cubin", "attn_fwd_vswap.cubin"]:
+for cub in ["attn_fwd.cubin"]:
     tgt = AttnTarget(B=1, H=2, S=512, cubin_file=cub).allocate()
     be = B200Backend(tgt)
     be.run_perm(None)
