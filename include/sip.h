@@ -44,6 +44,7 @@ typedef struct sip_ctx sip_ctx;
 typedef struct sip_kernel sip_kernel;
 typedef struct sip_chains sip_chains;
 typedef struct sip_module sip_module;
+typedef struct sip_results sip_results;
 
 /* one memory reference (reference deps.MemRef, deps.py:203-209) */
 typedef struct {
@@ -135,6 +136,16 @@ int sip_anneal(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds, i
 int sip_anneal_ex(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds, int32_t chains,
                   const uint16_t* start, sip_record* history, uint16_t* best, uint16_t* current,
                   sip_chain_summary* summary, uint16_t* champion, int32_t* champion_chain);
+
+/* same, but every chain's history and schedules stay on the device; only the
+ * summaries come back.  Results are pulled per chain range on demand (the
+ * public API's AnnealState materialises lazily).  A result set must be
+ * destroyed before its sip_kernel.                                       */
+int sip_anneal_keep(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds, int32_t chains,
+                    const uint16_t* start, sip_chain_summary* summary, sip_results** out);
+int sip_results_fetch(sip_results* r, int32_t first, int32_t count, sip_record* history,
+                      uint16_t* best, uint16_t* current);
+int sip_results_destroy(sip_results* r);
 
 /* ---- G2 step mode: external energy (any backend.measure) ------------- */
 int sip_chains_create(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds,

@@ -134,11 +134,13 @@ class AnnealState:
     def __init__(self, best: Kernel | None, best_energy: float, current: Kernel | None,
                  current_energy: float, baseline: float, unit: str, iterations: int, history=None,
                  *, records=None, temps=None, best_perm=None, current_perm=None, base=None,
-                 ambiguous: int = 0):
+                 ambiguous: int = 0, device=None, priced: int | None = None):
         self._best = best
         self._current = current
         self._base = base  # listing the permutations index into (kernels built on access)
-        self.current_perm = current_perm
+        self._device = device  # (DeviceResults, chain): records/schedules still in HBM
+        self._priced = priced
+        self._current_perm = current_perm
         self.best_energy = best_energy
         self.current_energy = current_energy
         self.baseline = baseline
@@ -147,8 +149,25 @@ class AnnealState:
         self._history = history
         self._records = records
         self._temps = temps
-        self.best_perm = best_perm
+        self._best_perm = best_perm
         self.ambiguous = ambiguous
+
+    def _pull(self) -> None:
+        if self._device is not None and self._records is None:
+            res, c = self._device
+            self._records, self._best_perm, self._current_perm = res.fetch(c)
+
+    @property
+    def best_perm(self):
+        if self._best_perm is None:
+            self._pull()
+        return self._best_perm
+
+    @property
+    def current_perm(self):
+        if self._current_perm is None:
+            self._pull()
+        return self._current_perm
 
     @property
     def best(self) -> Kernel:
@@ -165,12 +184,14 @@ class AnnealState:
     @property
     def history(self) -> list:
         if self._history is None:
+            self._pull()
             self._history = ([] if self._records is None
                              else records_to_history(self._records, self.baseline, self._temps))
         return self._history
 
     @property
     def records(self):
+        self._pull()
         return self._records
 
     @property
@@ -179,7 +200,9 @@ class AnnealState:
 
     @property
     def priced(self) -> int:
-        if self._records is None:
+        if self._priced is not None:
+            return self._priced
+        if self.records is None:
             return sum(1 for r in self.history if r.energy is not None)
         return int(np.count_nonzero(self._records["status"] <= ST_PRICED))
 
@@ -192,9 +215,62 @@ def _permuted(kernel: Kernel, perm) -> Kernel:
     return kernel.with_schedule(tuple(seq[int(i)] for i in perm))
 
 
+_TABLES: dict = {}  # (id(kernel), machine) -> (kernel, tables): listings are reused across calls
+
+
 def device_kernel(kernel: Kernel, machine: MachineConfig | None = None, tables: KernelTables | None = None):
-    tables = tables or KernelTables.build(kernel, machine)
+    if tables is None:
+        key = (id(kernel), repr(machine or MachineConfig()))
+        hit = _TABLES.get(key)
+        if hit is None or hit[0] is not kernel:
+            if len(_TABLES) >= 8:
+                _TABLES.pop(next(iter(_TABLES)))
+            hit = (kernel, KernelTables.build(kernel, machine))
+            _TABLES[key] = hit
+        tables = hit[1]
     return get_context().kernel(tables)
+
+
+class BatchStates:
+    """The AnnealStates of one fused launch, built on access (a read-only list).
+
+    Summaries (energies, baseline, priced counts) are on the host; records and
+    schedules stay in HBM until a state's history / best / current is read.
+    """
+
+    def __init__(self, kernel: Kernel, summ, res, temps):
+        self.kernel = kernel
+        self.summ = summ
+        self.res = res
+        self.temps = temps
+        self._states: dict = {}
+
+    def __len__(self) -> int:
+        return len(self.summ)
+
+    def __getitem__(self, c):
+        if isinstance(c, slice):
+            return [self[i] for i in range(*c.indices(len(self)))]
+        if c < 0:
+            c += len(self)
+        if not 0 <= c < len(self):
+            raise IndexError(c)
+        st = self._states.get(c)
+        if st is None:
+            sm = self.summ[c]
+            st = AnnealState(None, float(sm["best_energy"]), None, float(sm["current_energy"]),
+                             float(sm["t0"]), "cycles", len(self.temps), temps=self.temps,
+                             base=self.kernel, device=(self.res, c), priced=int(sm["priced"]),
+                             ambiguous=int(sm["ambiguous"]))
+            self._states[c] = st
+        return st
+
+    def __iter__(self):
+        return (self[i] for i in range(len(self)))
+
+    @property
+    def priced_total(self) -> int:
+        return int(self.summ["priced"].sum())
 
 
 def anneal_batch_sim(kernel: Kernel, machine: MachineConfig, cfg: AnnealConfig, seeds,
@@ -204,20 +280,11 @@ def anneal_batch_sim(kernel: Kernel, machine: MachineConfig, cfg: AnnealConfig, 
         raise NoCandidatesError("no global-memory instructions to move")
     dk = device_kernel(kernel, machine, tables)
     temps = cfg.temperatures()
-    hist, best, cur, summ = dk.anneal(seeds, temps, cfg.unsafe_moves, cfg.hw_safe,
-                                      cfg.min_fixed_distance, want_schedules=want_schedules)
-    out = []
-    for c in range(len(seeds)):
-        t0 = float(summ["t0"][c])
-        if t0 <= 0:
-            raise InvalidBaseline(f"baseline measurement {t0} is not positive")
-        out.append(AnnealState(None, float(summ["best_energy"][c]), None,
-                               float(summ["current_energy"][c]), t0, "cycles", len(temps),
-                               records=hist[c], temps=temps, base=kernel,
-                               best_perm=None if best is None else best[c],
-                               current_perm=None if cur is None else cur[c],
-                               ambiguous=int(summ["ambiguous"][c])))
-    return out
+    summ, res = dk.anneal_keep(seeds, temps, unsafe=cfg.unsafe_moves, hw_safe=cfg.hw_safe,
+                               min_fixed=cfg.min_fixed_distance)
+    if len(summ) and float(summ["t0"].min()) <= 0:
+        raise InvalidBaseline(f"baseline measurement {float(summ['t0'].min())} is not positive")
+    return BatchStates(kernel, summ, res, temps)
 
 
 def anneal_steps(kernel: Kernel, backend, cfg: AnnealConfig, seeds, *,

@@ -671,6 +671,11 @@ struct sip_chains {
   uint16_t* d_start = nullptr;
 };
 
+struct sip_results {
+  sip_kernel* k = nullptr;
+  sip_chains* ws = nullptr;
+};
+
 static int chains_alloc(sip_ctx* ctx, sip_kernel* k, const sip_anneal_cfg* cfg, int chains,
                         const int64_t* seeds, sip_chains* o) {
   Chains& s = o->s;
@@ -940,9 +945,11 @@ done:
   return rc;
 }
 
-int sip_anneal_ex(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds, int32_t chains,
-                  const uint16_t* start, sip_record* history, uint16_t* best, uint16_t* current,
-                  sip_chain_summary* summary, uint16_t* champion, int32_t* champion_chain) {
+}  // extern "C"
+
+// prepares the per-listing workspace and launches the fused kernel (no fetches)
+static int run_fused(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds, int32_t chains,
+                     const uint16_t* start, bool record_hist) {
   if (!k || !cfg || !seeds || chains < 1 || cfg->budget < 0) return SIP_E_ARG;
   sip_ctx* ctx = k->ctx;
   if (k->d.k == 0) return fail(ctx, SIP_E_NOCAND, "no global-memory instructions to move");
@@ -976,7 +983,7 @@ int sip_anneal_ex(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds
     TRY(dalloc(ctx, &k->d_base, MT_N));
     TRY(h2d(ctx, k->d_base, mt_base_host().data(), MT_N));
   }
-  o.s.record_hist = history != nullptr;
+  o.s.record_hist = record_hist ? 1 : 0;
   o.s.start = nullptr;
   if (start) {
     if (!o.d_start) TRY(dalloc(ctx, &o.d_start, (size_t)o.s.n));
@@ -990,6 +997,18 @@ int sip_anneal_ex(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds
       k->d, o.s, k->d_base, use_smem, (double)k->baseline);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ctx, SIP_E_CUDA, std::string("anneal: ") + cudaGetErrorString(e));
+  return SIP_OK;
+}
+
+extern "C" {
+
+int sip_anneal_ex(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds, int32_t chains,
+                  const uint16_t* start, sip_record* history, uint16_t* best, uint16_t* current,
+                  sip_chain_summary* summary, uint16_t* champion, int32_t* champion_chain) {
+  int rc = run_fused(k, cfg, seeds, chains, start, history != nullptr);
+  if (rc != SIP_OK) return rc;
+  sip_ctx* ctx = k->ctx;
+  sip_chains& o = *k->ws;
   std::vector<sip_chain_summary> tmp;
   sip_chain_summary* sum = summary;
   if (!sum && champion) {
@@ -1105,6 +1124,47 @@ int sip_chains_destroy(sip_chains* o) {
   if (!o) return SIP_OK;
   chains_free(o);
   delete o;
+  return SIP_OK;
+}
+
+int sip_anneal_keep(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds, int32_t chains,
+                    const uint16_t* start, sip_chain_summary* summary, sip_results** out) {
+  if (!summary || !out) return SIP_E_ARG;
+  int rc = run_fused(k, cfg, seeds, chains, start, true);
+  if (rc != SIP_OK) return rc;
+  TRY(chains_fetch(k->ws, nullptr, nullptr, nullptr, summary));
+  auto* r = new sip_results();
+  r->k = k;
+  r->ws = k->ws;  // the workspace now belongs to the result set
+  k->ws = nullptr;
+  *out = r;
+  return SIP_OK;
+}
+
+int sip_results_fetch(sip_results* r, int32_t first, int32_t count, sip_record* history, uint16_t* best,
+                      uint16_t* current) {
+  if (!r || !r->ws || first < 0 || count < 0 || first + count > r->ws->s.C) return SIP_E_ARG;
+  sip_ctx* ctx = r->k->ctx;
+  Chains& s = r->ws->s;
+  if (count == 0) return SIP_OK;
+  if (history) TRY(d2h(ctx, history, s.hist + (size_t)first * s.budget, (size_t)count * s.budget));
+  if (best) TRY(fetch_sched(ctx, s.best + (size_t)first * s.ns, s.n, s.ns, count, best));
+  if (current) TRY(fetch_sched(ctx, s.sched + (size_t)first * s.ns, s.n, s.ns, count, current));
+  SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return SIP_OK;
+}
+
+int sip_results_destroy(sip_results* r) {
+  if (!r) return SIP_OK;
+  if (r->ws) {
+    if (r->k && !r->k->ws) {
+      r->k->ws = r->ws;  // hand the buffers back for the next call
+    } else {
+      chains_free(r->ws);
+      delete r->ws;
+    }
+  }
+  delete r;
   return SIP_OK;
 }
 

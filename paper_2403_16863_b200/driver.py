@@ -37,6 +37,31 @@ class ChainOutcome:
         return True if self.verdict is None else self.verdict.ok
 
 
+class LazyOutcomes:
+    """ChainOutcomes of a batched simulator search, built on access (read-only list)."""
+
+    def __init__(self, states, seed0: int):
+        self.states = states
+        self.seed0 = seed0
+        self._items: dict = {}
+
+    def __len__(self) -> int:
+        return len(self.states)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(len(self)))]
+        if i < 0:
+            i += len(self)
+        o = self._items.get(i)
+        if o is None:
+            o = self._items[i] = ChainOutcome(self.seed0 + i, self.states[i], None)
+        return o
+
+    def __iter__(self):
+        return (self[i] for i in range(len(self)))
+
+
 @dataclass
 class SearchReport:
     kernel: Kernel
@@ -46,6 +71,14 @@ class SearchReport:
     chains: list
     best: ChainOutcome | None
     candidate_count: int = 0
+
+    @property
+    def candidates_evaluated(self) -> int:
+        """Priced proposals over all chains (history records with an energy)."""
+        st = getattr(self.chains, "states", None)
+        if st is not None and hasattr(st, "priced_total"):
+            return st.priced_total
+        return sum(o.state.priced for o in self.chains)
 
     @property
     def best_time(self) -> float | None:
@@ -101,6 +134,17 @@ def run_search(kernel: Kernel, backend, anneal_cfg: AnnealConfig, *, chains: int
     digest = input_hash(serialize_kernel(kernel))
     states = run_states(kernel, backend, anneal_cfg, chains, _tester(kernel, plan, anneal_cfg),
                         on_epoch=on_epoch)
+    if plan is None and store is None and hasattr(states, "summ"):
+        # batched simulator search: rank on the device summaries, build outcomes on access
+        import numpy as np
+
+        summ = states.summ
+        times = summ["best_energy"] * summ["t0"]
+        seeds = anneal_cfg.seed + np.arange(len(summ))
+        lazy = LazyOutcomes(states, anneal_cfg.seed)
+        best = lazy[int(np.lexsort((seeds, times))[0])] if len(summ) else None
+        baseline = float(summ["t0"][-1]) if len(summ) else 0.0
+        return SearchReport(kernel, digest, baseline, "cycles", lazy, best, len(candidates(kernel)))
     outcomes = []
     for c, st in enumerate(states):
         verdict = None

@@ -98,6 +98,11 @@ _SIGS = {
                     ctypes.c_void_p, c_u16p, c_u16p, ctypes.c_void_p], ctypes.c_int),
     "sip_anneal_ex": ([ctypes.c_void_p, ctypes.POINTER(AnnealCfg), c_i64p, ctypes.c_int32, c_u16p,
                        ctypes.c_void_p, c_u16p, c_u16p, ctypes.c_void_p, c_u16p, c_i32p], ctypes.c_int),
+    "sip_anneal_keep": ([ctypes.c_void_p, ctypes.POINTER(AnnealCfg), c_i64p, ctypes.c_int32, c_u16p,
+                         ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "sip_results_fetch": ([ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, c_u16p, c_u16p],
+                          ctypes.c_int),
+    "sip_results_destroy": ([ctypes.c_void_p], ctypes.c_int),
     "sip_chains_create": ([ctypes.c_void_p, ctypes.POINTER(AnnealCfg), c_i64p, c_dblp,
                            ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
     "sip_chains_propose": ([ctypes.c_void_p, c_i32p, c_u16p], ctypes.c_int),
@@ -333,9 +338,58 @@ class DeviceKernel:
             summ.ctypes.data_as(ctypes.c_void_p), _ptr(champ, c_u16p), ctypes.byref(wch)))
         return hist, summ, champ, wch.value
 
+    def anneal_keep(self, seeds, temps: np.ndarray, start=None, unsafe: bool = False,
+                    hw_safe: bool = False, min_fixed: int = 0):
+        """Fused chains whose histories and schedules stay on the device (sip_anneal_keep)."""
+        seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.int64))
+        temps = np.ascontiguousarray(temps, dtype=np.float64)
+        C = len(seeds)
+        summ = np.zeros(C, dtype=SUMMARY_DTYPE)
+        st = None if start is None else np.ascontiguousarray(start, dtype=np.uint16)
+        cfg = self._cfg(temps, unsafe, hw_safe, min_fixed)
+        h = ctypes.c_void_p()
+        self.ctx.check(self.ctx.lib.sip_anneal_keep(
+            self.handle, ctypes.byref(cfg), _ptr(seeds, c_i64p), C,
+            None if st is None else _ptr(st, c_u16p), summ.ctypes.data_as(ctypes.c_void_p), ctypes.byref(h)))
+        return summ, DeviceResults(self, h, C, len(temps))
+
     def chains(self, seeds, t0, temps: np.ndarray, unsafe: bool = False, hw_safe: bool = False,
                min_fixed: int = 0) -> "StepChains":
         return StepChains(self, seeds, t0, temps, unsafe, hw_safe, min_fixed)
+
+
+class DeviceResults:
+    """Per-chain histories and schedules left in HBM by sip_anneal_keep; fetched on demand."""
+
+    def __init__(self, dk: DeviceKernel, handle, chains: int, budget: int):
+        self.dk = dk  # keeps the listing (and its workspace) alive
+        self.handle = handle
+        self.C = chains
+        self.budget = budget
+        self._cache: dict = {}
+
+    def fetch(self, c: int):
+        """(records[budget], best[n], current[n]) of chain c."""
+        hit = self._cache.get(c)
+        if hit is not None:
+            return hit
+        n = self.dk.n
+        hist = np.zeros(self.budget, dtype=RECORD_DTYPE)
+        best = np.zeros(n, dtype=np.uint16)
+        cur = np.zeros(n, dtype=np.uint16)
+        ctx = self.dk.ctx
+        ctx.check(ctx.lib.sip_results_fetch(self.handle, c, 1, hist.ctypes.data_as(ctypes.c_void_p),
+                                            _ptr(best, c_u16p), _ptr(cur, c_u16p)))
+        self._cache[c] = (hist, best, cur)
+        return self._cache[c]
+
+    def __del__(self):
+        try:
+            if self.handle:
+                self.dk.ctx.lib.sip_results_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
 
 
 class StepChains:
