@@ -246,6 +246,7 @@ static int bit_get(const uint64_t* row, int b) { return (int)((row[b >> 6] >> (b
 
 #define FENCE_BIT (1u << 21)
 #define GLOBAL_BIT (1u << 22)
+#define CAND_BIT (1u << 23) /* movable: GLOBAL classes (reference) or the opt-in extension */
 
 static int alias(const sip_memref* a, const sip_memref* b) {
   if (a->space != 3 && b->space != 3 && a->space != b->space) return 0;
@@ -409,7 +410,7 @@ int oracle_anneal(const sip_tables* t, const double* temps, int budget, int unsa
   for (int i = 0; i < n; i++) x[i] = best[i] = (uint16_t)i;
   int k = 0;
   for (int i = 0; i < n; i++)
-    if (t->ctrl[i] & GLOBAL_BIT) k++;
+    if (t->ctrl[i] & CAND_BIT) k++;
   if (k == 0) {
     free(x); free(cand); free(best); free(adj); free(cpos);
     return SIP_E_NOCAND;
@@ -423,7 +424,7 @@ int oracle_anneal(const sip_tables* t, const double* temps, int budget, int unsa
   for (int it = 0; it < budget; it++) {
     int nc = 0; /* perturb.candidates: positions of global-class instructions */
     for (int p = 0; p < n; p++)
-      if (t->ctrl[x[p]] & GLOBAL_BIT) cpos[nc++] = p;
+      if (t->ctrl[x[p]] & CAND_BIT) cpos[nc++] = p;
     uint32_t cell = mt_below(&m, 2u * (uint32_t)nc);
     int ci = (int)(cell >> 1), dir = (int)(cell & 1u);
     int pos = cpos[ci];

@@ -61,6 +61,7 @@ class AnnealConfig:
     unsafe_moves: bool = False
     hw_safe: bool = False          # extension; False reproduces the reference
     min_fixed_distance: int = 8    # hw_safe: issue distance a fixed-latency RAW pair keeps
+    candidate_classes: str = "global"  # "extended": sm_100 extension; global = reference
 
     def __post_init__(self) -> None:
         if self.t_min <= 0 or self.t_max <= 0:
@@ -215,17 +216,18 @@ def _permuted(kernel: Kernel, perm) -> Kernel:
     return kernel.with_schedule(tuple(seq[int(i)] for i in perm))
 
 
-_TABLES: dict = {}  # (id(kernel), machine) -> (kernel, tables): listings are reused across calls
+_TABLES: dict = {}  # (id(kernel), machine, classes) -> (kernel, tables): listings are reused
 
 
-def device_kernel(kernel: Kernel, machine: MachineConfig | None = None, tables: KernelTables | None = None):
+def device_kernel(kernel: Kernel, machine: MachineConfig | None = None, tables: KernelTables | None = None,
+                  classes: str = "global"):
     if tables is None:
-        key = (id(kernel), repr(machine or MachineConfig()))
+        key = (id(kernel), repr(machine or MachineConfig()), classes)
         hit = _TABLES.get(key)
         if hit is None or hit[0] is not kernel:
             if len(_TABLES) >= 8:
                 _TABLES.pop(next(iter(_TABLES)))
-            hit = (kernel, KernelTables.build(kernel, machine))
+            hit = (kernel, KernelTables.build(kernel, machine, classes=classes))
             _TABLES[key] = hit
         tables = hit[1]
     return get_context().kernel(tables)
@@ -276,9 +278,9 @@ class BatchStates:
 def anneal_batch_sim(kernel: Kernel, machine: MachineConfig, cfg: AnnealConfig, seeds,
                      tables: KernelTables | None = None, want_schedules: bool = True) -> list:
     """Many simulator-energy chains in one launch; one AnnealState per seed."""
-    if len(candidates(kernel)) == 0:
+    if len(candidates(kernel, cfg.candidate_classes)) == 0:
         raise NoCandidatesError("no global-memory instructions to move")
-    dk = device_kernel(kernel, machine, tables)
+    dk = device_kernel(kernel, machine, tables, cfg.candidate_classes)
     temps = cfg.temperatures()
     summ, res = dk.anneal_keep(seeds, temps, unsafe=cfg.unsafe_moves, hw_safe=cfg.hw_safe,
                                min_fixed=cfg.min_fixed_distance)
@@ -295,7 +297,7 @@ def anneal_steps(kernel: Kernel, backend, cfg: AnnealConfig, seeds, *,
     All chains advance together; each round prices at most one candidate per
     chain.  ``on_epoch(chains, round)`` may exchange schedules between rounds.
     """
-    if len(candidates(kernel)) == 0:
+    if len(candidates(kernel, cfg.candidate_classes)) == 0:
         raise NoCandidatesError("no global-memory instructions to move")
     seeds = list(seeds)
     t0 = []
@@ -304,7 +306,7 @@ def anneal_steps(kernel: Kernel, backend, cfg: AnnealConfig, seeds, *,
         if v <= 0:
             raise InvalidBaseline(f"baseline measurement {v} is not positive")
         t0.append(v)
-    dk = device_kernel(kernel, MachineConfig(), tables)
+    dk = device_kernel(kernel, MachineConfig(), tables, cfg.candidate_classes)
     temps = cfg.temperatures()
     chains = dk.chains(seeds, t0, temps, cfg.unsafe_moves, cfg.hw_safe, cfg.min_fixed_distance)
     C = len(seeds)
@@ -353,5 +355,5 @@ def anneal(kernel: Kernel, backend, config: AnnealConfig | None = None, *,
     from .driver import hardware_config
 
     cfg = hardware_config(backend, cfg)
-    tables = backend.tables_for(kernel) if hasattr(backend, "tables_for") else None
+    tables = backend.tables_for(kernel, cfg.candidate_classes) if hasattr(backend, "tables_for") else None
     return anneal_steps(kernel, backend, cfg, [cfg.seed], tester=tester, tables=tables)[0]

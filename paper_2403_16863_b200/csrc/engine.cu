@@ -27,7 +27,8 @@ int fail(sip_ctx* ctx, int code, const std::string& msg) {
 }
 
 constexpr uint32_t FENCE_BIT = 1u << 21;
-constexpr uint32_t GLOBAL_BIT = 1u << 22;
+constexpr uint32_t GLOBAL_BIT = 1u << 22;  // global-memory class (memory-order semantics)
+constexpr uint32_t CAND_BIT = 1u << 23;    // movable candidate (perturb.candidates)
 
 __host__ __device__ __forceinline__ uint32_t c_wait(uint32_t c) { return c & 63u; }
 __host__ __device__ __forceinline__ uint32_t c_rd(uint32_t c) { return (c >> 6) & 7u; }
@@ -124,6 +125,9 @@ template <typename SchedAt>
 __device__ bool hw_safe_ok(const KernelDev& d, const uint2* meta, SchedAt at, int n, int lo, int a,
                            int b, int minfix) {
   if (d.pin[a] || d.pin[b]) return false;
+  // a scoreboard wait also acquires every earlier same-pipe result that ptxas left
+  // without a barrier (in-order completion): waiting instructions never move
+  if (c_wait(meta[a].x) || c_wait(meta[b].x)) return false;
   if (c_reuse(meta[a].x) || c_reuse(meta[b].x)) return false;
   if (lo > 0 && c_reuse(meta[at(lo - 1)].x)) return false;
   // producers P above: distance P -> b shrinks by adv(a)
@@ -799,7 +803,7 @@ int sip_kernel_create(sip_ctx* ctx, const sip_tables* t, sip_kernel** out) {
   std::vector<int32_t> gids;
   for (size_t i = 0; i < n; ++i) {
     meta[i] = make_uint2(t->ctrl[i], t->lat[i]);
-    if (t->ctrl[i] & GLOBAL_BIT) {
+    if (t->ctrl[i] & CAND_BIT) {
       gid[i] = (int16_t)gids.size();
       gids.push_back((int32_t)i);
     }

@@ -113,7 +113,7 @@ def run_states(kernel: Kernel, backend, cfg: AnnealConfig, chains: int, tester=N
                tables=None, on_epoch=None) -> list:
     cfg = hardware_config(backend, cfg)
     if tables is None and hasattr(backend, "tables_for"):
-        tables = backend.tables_for(kernel)
+        tables = backend.tables_for(kernel, cfg.candidate_classes)
     seeds = [cfg.seed + c for c in range(chains)]
     if tester is None and uses_device_energy(backend):
         return anneal_batch_sim(kernel, backend.machine, cfg, seeds, tables=tables)

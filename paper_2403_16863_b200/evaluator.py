@@ -70,7 +70,7 @@ class B200Backend:
     def min_fixed(self) -> int:
         return min_fixed_distance(self.listing.kernel)
 
-    def tables_for(self, kernel: Kernel):
+    def tables_for(self, kernel: Kernel, classes: str = "global"):
         """Device tables of `kernel` (a permutation of the listing) with the cubin's
         reuse bits and pinned instructions attached to each identity."""
         from .machine import MachineConfig
@@ -79,7 +79,7 @@ class B200Backend:
         ids = schedule_perm(kernel)
         reuse = [self.listing.reuse[int(i)] for i in ids]
         pinned = [p for p, i in enumerate(ids) if self.listing.pins[int(i)]]
-        return KernelTables.build(kernel, MachineConfig(), reuse=reuse, pinned=pinned)
+        return KernelTables.build(kernel, MachineConfig(), reuse=reuse, pinned=pinned, classes=classes)
 
     def perm_of(self, kernel: Kernel) -> np.ndarray:
         return schedule_perm(kernel)

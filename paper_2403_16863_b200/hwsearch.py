@@ -31,7 +31,7 @@ class HardwareSearch:
         self.be = backend
         self.cfg = hardware_config(backend, cfg)
         self.kernel = backend.kernel
-        self.tables = backend.tables_for(self.kernel)
+        self.tables = backend.tables_for(self.kernel, self.cfg.candidate_classes)
         self.dk = backend.ctx.kernel(self.tables)
         self.dist = dist  # torch.distributed module when world_size > 1
         self.rank = dist.get_rank() if dist else 0
