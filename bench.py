@@ -58,7 +58,8 @@ def parse():
     ap.add_argument("--chains", type=int, default=8, help="hardware-priced chains per GPU")
     ap.add_argument("--hw-steps", type=int, default=8, help="hardware search rounds")
     ap.add_argument("--epoch", type=int, default=8, help="rounds between global-best exchanges")
-    ap.add_argument("--verify-samples", type=int, default=200_000)
+    ap.add_argument("--verify-samples", type=int, default=10_000_000,
+                    help="samples per accepted (champion) schedule, sharded over ranks")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-attn", action="store_true")
@@ -252,6 +253,7 @@ def hardware_phase(kind, listing, local, rank, world, dist, args, rounds):
 
     MAX = dist.ReduceOp.MAX if dist else None
     SUM = dist.ReduceOp.SUM if dist else None
+    MIN = dist.ReduceOp.MIN if dist else None
     shape = SHAPE if kind == "gemm" else ATTN_SHAPE
     tgt = make_target(kind, device=local, **shape).allocate()
     be = B200Backend(tgt, listing, device=local, warmup=2, flush_l2=True)
@@ -273,6 +275,9 @@ def hardware_phase(kind, listing, local, rank, world, dist, args, rounds):
     clocks = hclk.summary()
     h_ms = allreduce(dist, [h0.elapsed_time(h1)], MAX)[0]
     h_eval, h_launch = allreduce(dist, [hs.evaluated - evald0, hs.launches - launches0], SUM)
+    # the nvcc schedule timed on its own as well, so the roofline never depends on how
+    # many candidates the search happened to price
+    be._measure_single(np.arange(n, dtype=np.uint16), 15)
     kern = list(be.kernel_ms)
     pk = peaks()
     avg_ms = sum(kern) / len(kern)
@@ -294,6 +299,7 @@ def hardware_phase(kind, listing, local, rank, world, dist, args, rounds):
                 else "fallback 1590 TFLOP/s"}
     floor_ms = (2 if be.paired else 1) * (be.warmup + hcfg.measure_reps) * avg_ms
     hw = {"candidates_per_s": h_eval / (h_ms / 1e3), "rounds": rounds, "chains_per_gpu": args.chains,
+          "proposals": rounds * args.chains * world, "priced": int(h_eval),
           "evaluator_roofline_candidates_per_s": world * 1e3 / floor_ms,
           "device_busy_frac": (h_eval / (h_ms / 1e3)) / (world * 1e3 / floor_ms),
           "note": "one candidate = re-encode + cuModuleLoadData + one CUDA graph of 2 warmup + 5 timed "
@@ -317,12 +323,27 @@ def hardware_phase(kind, listing, local, rank, world, dist, args, rounds):
                  "instructions_moved": int((best != ident).sum()),
                  "search_best_energy": res["best_energy"],
                  "paper_speedup": 1.1227 if kind == "gemm" else 1.062}
-        ver = Verifier(kind, device=local)
-        vr = ver.run(best, args.verify_samples)
-        verify = {"samples": vr.samples, "passed": vr.passed, "failed": vr.failed,
-                  "bit_identical": vr.bitdiff_elems == 0, "seconds": vr.seconds,
+    # every rank verifies its share of the samples (batches rank, rank+world, ...) of the
+    # same champion; (passed, failed) sum and the first failing sample is the min over ranks
+    best = res["best_perm"]
+    if dist:
+        bt = torch.from_numpy(best.astype(np.int32)).cuda()
+        dist.broadcast(bt, 0)
+        best = bt.cpu().numpy().astype(np.uint16)
+    ver = Verifier(kind, device=local)
+    per_rank = -(-args.verify_samples // (world * ver.batch)) * ver.batch
+    vr = ver.run(best, per_rank, first_batch=rank, batch_stride=world)
+    tot = allreduce(dist, [vr.samples, vr.passed, vr.failed, vr.bitdiff_elems, vr.compared_bytes], SUM)
+    vsec = allreduce(dist, [vr.seconds], MAX)[0]
+    ff = allreduce(dist, [vr.first_fail_sample if vr.first_fail_sample >= 0 else 2.0 ** 62], MIN)[0]
+    if rank == 0:
+        verify = {"samples": int(tot[0]), "passed": int(tot[1]), "failed": int(tot[2]),
+                  "bit_identical": tot[3] == 0, "first_failing_sample": None if ff >= 2.0 ** 62 else int(ff),
+                  "seconds": vsec, "samples_per_s": tot[0] / vsec,
+                  "compare_gb_per_s": tot[4] / vsec / 1e9, "ranks": world,
                   "sample": ("one independent 256x256x1024 GEMM+LeakyReLU problem" if kind == "gemm"
-                             else "one independent head, S=256 D=128") + ", Philox inputs",
+                             else "one independent head, S=256 D=128") + ", Philox inputs; baseline "
+                            "and champion launched on it, outputs compared (sip_compare)",
                   "tolerance": {"atol": ver.atol, "rtol": ver.rtol}}
     return {"roofline": roofline, "hw": hw, "tuned": tuned, "verify": verify, "launches": h_launch}
 

@@ -202,6 +202,9 @@ int sip_measure_paired(sip_module* m, const uint16_t* perm_ref, const uint16_t* 
                        double* raw_ratio);
 /* run the permuted module once on the given launch (verification) */
 int sip_run(sip_module* m, const uint16_t* perm, const sip_launch* launch);
+/* same, enqueued on the context stream without synchronising (errors surface at
+ * the next synchronising call, e.g. sip_verify_result)                      */
+int sip_run_async(sip_module* m, const uint16_t* perm, const sip_launch* launch);
 
 /* ---- G5/G6: probabilistic verification --------------------------------
  * replaces difftest.sample_inputs / run_tests compare (difftest.py:124-204) */
@@ -221,6 +224,18 @@ int sip_fill_normal(sip_ctx* ctx, void* dev, size_t count, int32_t dtype, uint64
 int sip_compare(sip_ctx* ctx, const void* ref, const void* cand, size_t count, int32_t dtype,
                 double atol, double rtol, int64_t elems_per_sample, int64_t first_sample,
                 sip_cmp_result* out);
+/* accumulating compare for long verification runs (10M samples):
+ * sip_verify_compare enqueues one batch (count elements = count/elems_per_sample
+ * samples starting at global sample index first_sample) without synchronising;
+ * sip_verify_result synchronises and reports the totals so far (first failure
+ * as a global sample index, min over batches).  run_tests' verdict fields,
+ * difftest.py:158-204.                                                      */
+typedef struct sip_verify_acc sip_verify_acc;
+int sip_verify_open(sip_ctx* ctx, int64_t max_samples, int64_t elems_per_sample, sip_verify_acc** out);
+int sip_verify_compare(sip_verify_acc* acc, const void* ref, const void* cand, size_t count, int32_t dtype,
+                       double atol, double rtol, int64_t first_sample);
+int sip_verify_result(sip_verify_acc* acc, sip_cmp_result* out);
+int sip_verify_close(sip_verify_acc* acc);
 /* difftest.sample_inputs (difftest.py:124-141): CPython Random(f"{seed}:{s}")
  * streams generated on the device.  spec = (nbytes, cell, dist) per buffer
  * (dist 0 uniform, 1 small, 2 zero); out = [count][sum nbytes] host bytes. */

@@ -377,6 +377,14 @@ int sip_run(sip_module* m, const uint16_t* perm, const sip_launch* L) {
   return SIP_OK;
 }
 
+int sip_run_async(sip_module* m, const uint16_t* perm, const sip_launch* L) {
+  if (!m || !L || !m->ctx) return SIP_E_ARG;
+  CachedMod* cm = nullptr;
+  int rc = get_module(m, perm, &cm);
+  if (rc != SIP_OK) return rc;
+  return launch(m, cm, L);
+}
+
 // warmup launches of every module, then `reps` rounds; round r launches the
 // modules in rotated order (ABAB.. / BABA..), each bracketed by an event pair
 // and preceded by an optional L2 flush.  Everything runs from one CUDA graph.

@@ -8,8 +8,8 @@
 
 namespace {
 
-constexpr uint32_t kGemmOffsets[8] = {0, 128, 256, 264, 268, 272, 276, 280};
-constexpr uint32_t kGemmParamBytes = 284;
+constexpr uint32_t kGemmOffsets[9] = {0, 128, 256, 384, 392, 396, 400, 404, 408};
+constexpr uint32_t kGemmParamBytes = 412;
 constexpr uint32_t kAttnOffsets[9] = {0, 128, 256, 384, 392, 396, 400, 404, 408};
 constexpr uint32_t kAttnParamBytes = 412;
 
@@ -42,18 +42,24 @@ int sip_target_gemm_launch(sip_ctx* ctx, const void* A, const void* B, void* C, 
   cuuint64_t db[3] = {(cuuint64_t)K, (cuuint64_t)N, (cuuint64_t)L};
   cuuint64_t sb[2] = {(cuuint64_t)K * 2, (cuuint64_t)N * K * 2};
   cuuint32_t bb[3] = {64, 256, 1};
+  cuuint32_t bh[3] = {64, 128, 1};  // half-width B box for the 128x128 tail tiles
   int rc = encode(ctx, reinterpret_cast<CUtensorMap*>(p), A, 3, da, sa, ba);
   if (rc == SIP_OK) rc = encode(ctx, reinterpret_cast<CUtensorMap*>(p + 128), B, 3, db, sb, bb);
+  if (rc == SIP_OK) rc = encode(ctx, reinterpret_cast<CUtensorMap*>(p + 256), B, 3, db, sb, bh);
   if (rc != SIP_OK) return rc;
-  std::memcpy(p + 256, &C, 8);
-  std::memcpy(p + 264, &M, 4);
-  std::memcpy(p + 268, &N, 4);
-  std::memcpy(p + 272, &K, 4);
-  std::memcpy(p + 276, &L, 4);
-  std::memcpy(p + 280, &slope, 4);
+  std::memcpy(p + 384, &C, 8);
+  std::memcpy(p + 392, &M, 4);
+  std::memcpy(p + 396, &N, 4);
+  std::memcpy(p + 400, &K, 4);
+  std::memcpy(p + 404, &L, 4);
+  std::memcpy(p + 408, &slope, 4);
+  // persistent grid: one CTA per SM; problems with at most half as many tiles as SMs
+  // run every tile as two 128x128 halves (see the kernel's Schedule)
   long tiles = (long)(M / 128) * (N / 256) * L;
+  long sms = ctx->sm_count;
+  long grid = tiles >= sms ? sms : (2 * tiles <= sms ? 2 * tiles : tiles);
   std::memset(launch, 0, sizeof *launch);
-  launch->grid[0] = (uint32_t)(tiles < ctx->sm_count ? tiles : ctx->sm_count);
+  launch->grid[0] = (uint32_t)grid;
   launch->grid[1] = launch->grid[2] = 1;
   launch->block[0] = 192;
   launch->block[1] = launch->block[2] = 1;
@@ -61,7 +67,7 @@ int sip_target_gemm_launch(sip_ctx* ctx, const void* A, const void* B, void* C, 
   launch->smem_bytes = 4 * (128 * 64 * 2 + 256 * 64 * 2) + 1024 + 256;
   launch->params = params;
   launch->param_offsets = kGemmOffsets;
-  launch->nparams = 8;
+  launch->nparams = 9;
   launch->params_size = kGemmParamBytes;
   return SIP_OK;
 }

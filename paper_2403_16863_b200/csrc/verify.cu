@@ -97,7 +97,7 @@ __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return _
 template <typename T>
 __device__ __forceinline__ void cmp_elem(T a, T b, float atol, float rtol, size_t idx, int& mis,
                                          int& bits, float& err, unsigned long long& first,
-                                         uint8_t* flags, int64_t eps) {
+                                         uint8_t* flags, int64_t eps, unsigned long long elem_base) {
   unsigned short ua = *reinterpret_cast<unsigned short*>(&a), ub = *reinterpret_cast<unsigned short*>(&b);
   if (ua == ub) return;
   ++bits;
@@ -113,7 +113,7 @@ __device__ __forceinline__ void cmp_elem(T a, T b, float atol, float rtol, size_
   }
   if (bad) {
     ++mis;
-    if (idx < first) first = idx;
+    if (idx + elem_base < first) first = idx + elem_base;
     flags[idx / eps] = 1;
   }
 }
@@ -137,7 +137,8 @@ __device__ __forceinline__ float warp_max(float v) {
 template <typename T>
 __global__ void __launch_bounds__(256) compare_kernel(const T* __restrict__ ref, const T* __restrict__ cand,
                                                       size_t count, float atol, float rtol, int64_t eps,
-                                                      uint8_t* flags, CmpAcc* acc) {
+                                                      uint8_t* flags, CmpAcc* acc,
+                                                      unsigned long long elem_base) {
   constexpr int kVec = 8;     // elements per 16-byte load
   constexpr int kUnroll = 4;  // independent 16-byte loads in flight per operand
   int mis = 0, bits = 0;
@@ -166,11 +167,12 @@ __global__ void __launch_bounds__(256) compare_kernel(const T* __restrict__ ref,
       const T* a = reinterpret_cast<const T*>(&ra[u]);
       const T* b = reinterpret_cast<const T*>(&ca[u]);
 #pragma unroll
-      for (int i = 0; i < kVec; ++i) cmp_elem(a[i], b[i], atol, rtol, v * kVec + i, mis, bits, err, first, flags, eps);
+      for (int i = 0; i < kVec; ++i) cmp_elem(a[i], b[i], atol, rtol, v * kVec + i, mis, bits, err, first, flags, eps,
+                                     elem_base);
     }
   }
   for (size_t e = nvec * kVec + tid; e < count; e += stride)  // tail
-    cmp_elem(ref[e], cand[e], atol, rtol, e, mis, bits, err, first, flags, eps);
+    cmp_elem(ref[e], cand[e], atol, rtol, e, mis, bits, err, first, flags, eps, elem_base);
   unsigned long long m = warp_sum((unsigned long long)mis), b = warp_sum((unsigned long long)bits);
   unsigned long long f = warp_min(first);
   float me = warp_max(err);
@@ -287,11 +289,12 @@ int sip_compare(sip_ctx* ctx, const void* ref, const void* cand, size_t count, i
   int blocks = ctx->sm_count * 8;
   if (dtype == 0)
     compare_kernel<__half><<<blocks, 256, 0, ctx->stream>>>((const __half*)ref, (const __half*)cand, count,
-                                                            (float)atol, (float)rtol, elems_per_sample, flags, acc);
+                                                            (float)atol, (float)rtol, elems_per_sample, flags, acc,
+                                                            0ull);
   else
     compare_kernel<__nv_bfloat16><<<blocks, 256, 0, ctx->stream>>>(
         (const __nv_bfloat16*)ref, (const __nv_bfloat16*)cand, count, (float)atol, (float)rtol,
-        elems_per_sample, flags, acc);
+        elems_per_sample, flags, acc, 0ull);
   SIP_CHECK_LAUNCH(ctx);
   count_flags_kernel<<<ctx->sm_count, 256, 0, ctx->stream>>>(flags, nsamples, nfail);
   SIP_CHECK_LAUNCH(ctx);
@@ -317,6 +320,108 @@ int sip_compare(sip_ctx* ctx, const void* ref, const void* cand, size_t count, i
   float me;
   std::memcpy(&me, &h.max_err_bits, sizeof me);
   out->max_abs_err = (double)me;
+  return SIP_OK;
+}
+
+// ---- accumulating verification (no host synchronisation per batch) ----------
+// One accumulator per verification run: every batch's compare adds into the same
+// device counters, marks failing samples in a flag array indexed by the run's own
+// sample counter, and tracks the first failure as a global element index
+// (sample * elems_per_sample + element), so rank-strided batches merge by min.
+}  // extern "C"
+
+struct sip_verify_acc {
+  sip_ctx* ctx;
+  CmpAcc* acc;
+  uint8_t* flags;
+  unsigned long long* nfail;
+  int64_t max_samples, eps, used;
+};
+
+extern "C" {
+
+int sip_verify_open(sip_ctx* ctx, int64_t max_samples, int64_t elems_per_sample, sip_verify_acc** out) {
+  if (!ctx || !out || max_samples < 1 || elems_per_sample < 1) return SIP_E_ARG;
+  auto* a = new sip_verify_acc{ctx, nullptr, nullptr, nullptr, max_samples, elems_per_sample, 0};
+  cudaError_t e = cudaMalloc(&a->acc, sizeof(CmpAcc));
+  if (e == cudaSuccess) e = cudaMalloc(&a->flags, (size_t)max_samples);
+  if (e == cudaSuccess) e = cudaMalloc(&a->nfail, sizeof(unsigned long long));
+  if (e != cudaSuccess) {
+    cudaFree(a->acc);
+    cudaFree(a->flags);
+    delete a;
+    return sip::fail(ctx, SIP_E_CUDA, std::string("verify accumulator: ") + cudaGetErrorString(e));
+  }
+  CmpAcc init{0, 0, 0, ~0ull, 0};
+  SIP_CUDA(ctx, cudaMemcpyAsync(a->acc, &init, sizeof init, cudaMemcpyHostToDevice, ctx->stream));
+  SIP_CUDA(ctx, cudaMemsetAsync(a->flags, 0, (size_t)max_samples, ctx->stream));
+  SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  *out = a;
+  return SIP_OK;
+}
+
+int sip_verify_compare(sip_verify_acc* a, const void* ref, const void* cand, size_t count, int32_t dtype,
+                       double atol, double rtol, int64_t first_sample) {
+  if (!a || !ref || !cand || first_sample < 0) return SIP_E_ARG;
+  sip_ctx* ctx = a->ctx;
+  if ((reinterpret_cast<uintptr_t>(ref) | reinterpret_cast<uintptr_t>(cand)) & 15)
+    return sip::fail(ctx, SIP_E_ARG, "buffers must be 16-byte aligned");
+  const int64_t ns = (int64_t)((count + a->eps - 1) / a->eps);
+  if (a->used + ns > a->max_samples) return sip::fail(ctx, SIP_E_ARG, "verify accumulator is full");
+  const unsigned long long base = (unsigned long long)first_sample * (unsigned long long)a->eps;
+  int blocks = ctx->sm_count * 8;
+  if (dtype == 0)
+    compare_kernel<__half><<<blocks, 256, 0, ctx->stream>>>((const __half*)ref, (const __half*)cand, count,
+                                                            (float)atol, (float)rtol, a->eps,
+                                                            a->flags + a->used, a->acc, base);
+  else
+    compare_kernel<__nv_bfloat16><<<blocks, 256, 0, ctx->stream>>>(
+        (const __nv_bfloat16*)ref, (const __nv_bfloat16*)cand, count, (float)atol, (float)rtol, a->eps,
+        a->flags + a->used, a->acc, base);
+  SIP_CHECK_LAUNCH(ctx);
+  a->used += ns;
+  return SIP_OK;
+}
+
+int sip_verify_result(sip_verify_acc* a, sip_cmp_result* out) {
+  if (!a || !out) return SIP_E_ARG;
+  sip_ctx* ctx = a->ctx;
+  SIP_CUDA(ctx, cudaMemsetAsync(a->nfail, 0, sizeof(unsigned long long), ctx->stream));
+  if (a->used > 0) {
+    count_flags_kernel<<<ctx->sm_count, 256, 0, ctx->stream>>>(a->flags, (size_t)a->used, a->nfail);
+    SIP_CHECK_LAUNCH(ctx);
+  }
+  CmpAcc h;
+  unsigned long long nf = 0;
+  SIP_CUDA(ctx, cudaMemcpyAsync(&h, a->acc, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+  SIP_CUDA(ctx, cudaMemcpyAsync(&nf, a->nfail, sizeof nf, cudaMemcpyDeviceToHost, ctx->stream));
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess)
+    return sip::fail(ctx, SIP_E_MEASURE, std::string("verification batch: ") + cudaGetErrorString(e));
+  out->checked_elems = a->used * a->eps;
+  out->mismatched_elems = (int64_t)h.mismatched;
+  out->bitdiff_elems = (int64_t)h.bitdiff;
+  out->failed_samples = (int64_t)nf;
+  if (h.first != ~0ull) {
+    out->first_fail_sample = (int64_t)(h.first / (unsigned long long)a->eps);
+    out->first_fail_elem = (int64_t)(h.first % (unsigned long long)a->eps);
+  } else {
+    out->first_fail_sample = -1;
+    out->first_fail_elem = -1;
+  }
+  float me;
+  std::memcpy(&me, &h.max_err_bits, sizeof me);
+  out->max_abs_err = (double)me;
+  return SIP_OK;
+}
+
+int sip_verify_close(sip_verify_acc* a) {
+  if (!a) return SIP_OK;
+  cudaStreamSynchronize(a->ctx->stream);
+  cudaFree(a->acc);
+  cudaFree(a->flags);
+  cudaFree(a->nfail);
+  delete a;
   return SIP_OK;
 }
 

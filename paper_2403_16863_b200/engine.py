@@ -122,6 +122,13 @@ _SIGS = {
     "sip_measure_paired": ([ctypes.c_void_p, c_u16p, c_u16p, ctypes.POINTER(Launch), ctypes.c_int32,
                             ctypes.c_int32, ctypes.c_int32, c_dblp, c_dblp, c_dblp, c_dblp], ctypes.c_int),
     "sip_run": ([ctypes.c_void_p, c_u16p, ctypes.POINTER(Launch)], ctypes.c_int),
+    "sip_run_async": ([ctypes.c_void_p, c_u16p, ctypes.POINTER(Launch)], ctypes.c_int),
+    "sip_verify_open": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p)],
+                        ctypes.c_int),
+    "sip_verify_compare": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int32,
+                            ctypes.c_double, ctypes.c_double, ctypes.c_int64], ctypes.c_int),
+    "sip_verify_result": ([ctypes.c_void_p, ctypes.POINTER(CmpResult)], ctypes.c_int),
+    "sip_verify_close": ([ctypes.c_void_p], ctypes.c_int),
     "sip_fill_normal": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int32,
                          ctypes.c_uint64, ctypes.c_uint64, ctypes.c_float], ctypes.c_int),
     "sip_compare": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int32,

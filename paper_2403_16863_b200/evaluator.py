@@ -126,7 +126,13 @@ class B200Backend:
     def measure(self, kernel: Kernel, reps: int = 5) -> CostSample:
         if len(kernel.schedule) != self.listing.n:
             raise MeasurementFailed("schedule does not match the loaded cubin")
-        return self.measure_perm(self.perm_of(kernel), reps)
+        try:
+            perm = self.perm_of(kernel)
+        except ValueError as exc:
+            raise MeasurementFailed(f"schedule is not a listing of the loaded cubin: {exc}") from None
+        if not np.array_equal(np.sort(perm), self.identity):
+            raise MeasurementFailed("schedule is not a permutation of the loaded cubin's instructions")
+        return self.measure_perm(perm, reps)
 
     def run_perm(self, perm) -> None:
         perm = None if perm is None else np.ascontiguousarray(perm, dtype=np.uint16)

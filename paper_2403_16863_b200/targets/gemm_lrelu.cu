@@ -4,6 +4,11 @@
 // sm_100a instead of Triton/A100:
 //   * persistent: one CTA per SM, static round-robin over 128x256 output tiles
 //     (batched over L independent problems, used by the verifier);
+//   * wave-quantisation tail: when the last round of tiles would leave more than
+//     half the SMs idle (4096^3: 512 tiles on 148 SMs, last wave 46 % full), those
+//     tiles are split into two 128x128 halves (N=128 MMA, half-height B box), so
+//     the tail costs half a tile instead of a full one.  Small problems with fewer
+//     than half as many tiles as SMs run as half tiles throughout;
 //   * warp 0: TMA producer (SWIZZLE_128B, 4-stage 48 KB ring, mbarrier full/empty);
 //   * warp 1: TMEM allocator + single-thread tcgen05.mma issuer (M128 N256 K16),
 //     accumulating in one of two 256-column TMEM buffers;
@@ -23,11 +28,39 @@ constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE_BYTES = A_BYTE
 constexpr int ACC_COLS = BN, TMEM_COLS = 2 * ACC_COLS;
 constexpr int NUM_THREADS = 192;
 constexpr uint32_t IDESC = sm100::idesc_f16(BM, BN);
+constexpr uint32_t IDESC_HALF = sm100::idesc_f16(BM, BN / 2);
+
+// Work item t of the static schedule -> (problem l, m0, n0, half?).
+struct Schedule {
+  int tiles_m, tiles_n, full, items;
+  __device__ Schedule(int M, int N, int L, int grid) {
+    tiles_m = M / BM;
+    tiles_n = N / BN;
+    const int tiles = tiles_m * tiles_n * L;
+    const int rem = tiles % grid;
+    if (2 * tiles <= grid) {
+      full = 0;  // few tiles: every tile as two halves
+    } else if (tiles > grid && rem != 0 && 2 * rem <= grid) {
+      full = tiles - rem;  // whole waves of full tiles, tail as halves
+    } else {
+      full = tiles;
+    }
+    items = full + 2 * (tiles - full);
+  }
+  __device__ bool half(int t) const { return t >= full; }
+  __device__ void coords(int t, int& l, int& m0, int& n0) const {
+    const int tile = t < full ? t : full + ((t - full) >> 1);
+    l = tile / (tiles_m * tiles_n);
+    const int r = tile % (tiles_m * tiles_n);
+    m0 = (r / tiles_n) * BM;
+    n0 = (r % tiles_n) * BN + (t < full ? 0 : ((t - full) & 1) * (BN / 2));
+  }
+};
 }  // namespace
 
 extern "C" __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_lrelu_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-               __half* __restrict__ C, int M, int N, int K, int L, float slope) {
+               const __grid_constant__ CUtensorMap tmBh, __half* __restrict__ C, int M, int N, int K, int L, float slope) {
   using namespace sm100;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -41,12 +74,14 @@ gemm_lrelu_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 
   const int warp = warp_id();
   const int lane = threadIdx.x & 31;
-  const int tiles_m = M / BM, tiles_n = N / BN, kblocks = K / BK;
-  const int tiles = tiles_m * tiles_n * L;
+  const int kblocks = K / BK;
+  const Schedule sched(M, N, L, gridDim.x);
+  const int items = sched.items;
 
   if (warp == 0 && elect_one()) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
+    tma_prefetch(&tmBh);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -68,14 +103,16 @@ gemm_lrelu_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        int l = t / (tiles_m * tiles_n), r = t % (tiles_m * tiles_n);
-        int m0 = (r / tiles_n) * BM, n0 = (r % tiles_n) * BN;
+      for (int t = blockIdx.x; t < items; t += gridDim.x) {
+        int l, m0, n0;
+        sched.coords(t, l, m0, n0);
+        const bool half = sched.half(t);
+        const CUtensorMap* mb = half ? &tmBh : &tmB;
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], STAGE_BYTES);
+          mbar_expect_tx(&full[stage], half ? A_BYTES + B_BYTES / 2 : STAGE_BYTES);
           tma_load_3d(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, m0, l);
-          tma_load_3d(sB + stage * B_BYTES, &tmB, &full[stage], kb * BK, n0, l);
+          tma_load_3d(sB + stage * B_BYTES, mb, &full[stage], kb * BK, n0, l);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -88,9 +125,10 @@ gemm_lrelu_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     int stage = 0;
     uint32_t phase = 0;
     int local = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+    for (int t = blockIdx.x; t < items; t += gridDim.x, ++local) {
       const int buf = local & 1;
       const uint32_t use = local >> 1;
+      const uint32_t idesc = sched.half(t) ? IDESC_HALF : IDESC;
       mbar_wait(&acc_empty[buf], (use & 1) ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem + buf * ACC_COLS;
@@ -101,7 +139,7 @@ gemm_lrelu_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           const uint32_t a0 = smem_u32(sA + stage * A_BYTES), b0 = smem_u32(sB + stage * B_BYTES);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk)
-            mma_f16(d_tmem, desc_sw128(a0 + kk * 32), desc_sw128(b0 + kk * 32), IDESC, (kb | kk) != 0);
+            mma_f16(d_tmem, desc_sw128(a0 + kk * 32), desc_sw128(b0 + kk * 32), idesc, (kb | kk) != 0);
           mma_commit(&empty[stage]);
           if (kb == kblocks - 1) mma_commit(&acc_full[buf]);
         }
@@ -117,17 +155,18 @@ gemm_lrelu_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int row_in_tile = quarter * 32 + lane;
     int local = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+    for (int t = blockIdx.x; t < items; t += gridDim.x, ++local) {
       const int buf = local & 1;
       const uint32_t use = local >> 1;
-      int l = t / (tiles_m * tiles_n), r = t % (tiles_m * tiles_n);
-      int m0 = (r / tiles_n) * BM, n0 = (r % tiles_n) * BN;
+      int l, m0, n0;
+      sched.coords(t, l, m0, n0);
+      const int chunks = sched.half(t) ? BN / 64 : BN / 32;
       mbar_wait(&acc_full[buf], use & 1);
       tc_fence_after();
       __half* crow = C + ((size_t)l * M + m0 + row_in_tile) * (size_t)N + n0;
       const uint32_t t_base = tmem + ((uint32_t)(quarter * 32) << 16) + buf * ACC_COLS;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = 0; c < chunks; ++c) {
         uint32_t v[32];
         tmem_ld32(t_base + c * 32, v);
         tmem_ld_wait();

@@ -88,36 +88,45 @@ class Verifier:
         self.ctx.check(rc)
 
     def run(self, perm, samples: int, *, first_batch: int = 0, batch_stride: int = 1,
-            fail_fast: bool = False) -> VerifyResult:
-        """Verify `perm` on batches first_batch, first_batch+stride, ... covering `samples`."""
+            fail_fast: bool = False, check_every: int = 64) -> VerifyResult:
+        """Verify `perm` on batches first_batch, first_batch+stride, ... covering `samples`
+        (rounded up to whole batches).  Every batch is enqueued without a host round trip:
+        fill (Philox stream = batch index), baseline launch, candidate launch, and an
+        accumulating compare; the host synchronises every `check_every` batches (and
+        stops early on a failure when `fail_fast`) and once at the end."""
         t0 = time.perf_counter()
-        nb = (samples + self.batch - 1) // self.batch
-        passed = failed = bitdiff = mism = 0
-        first_s, first_e, maxerr = -1, -1, 0.0
-        done = 0
+        nb = max(1, (samples + self.batch - 1) // self.batch)
         lib = self.ctx.lib
+        p = None if perm is None else np.ascontiguousarray(perm, dtype=np.uint16)
+        pp = None if p is None else p.ctypes.data_as(c_u16p)
+        acc = ctypes.c_void_p()
+        self.ctx.check(lib.sip_verify_open(self.ctx.handle, nb * self.batch, self.elems_per_sample,
+                                           ctypes.byref(acc)))
         res = CmpResult()
-        for i in range(nb):
-            j = first_batch + i * batch_stride
-            self.target.fill(stream=j)
-            self._run(None, self.launch_ref)
-            self._run(perm, self.launch_cand)
-            rc = lib.sip_compare(self.ctx.handle, ctypes.c_void_p(self.out_ref.data_ptr()),
-                                 ctypes.c_void_p(self.out_cand.data_ptr()), self.out_ref.numel(), 0,
-                                 self.atol, self.rtol, self.elems_per_sample, j * self.batch,
-                                 ctypes.byref(res))
-            self.ctx.check(rc)
-            n_here = min(self.batch, samples - done)
-            done += n_here
-            failed += min(res.failed_samples, n_here)
-            passed += n_here - min(res.failed_samples, n_here)
-            bitdiff += res.bitdiff_elems
-            mism += res.mismatched_elems
-            maxerr = max(maxerr, res.max_abs_err)
-            if res.first_fail_sample >= 0 and (first_s < 0 or res.first_fail_sample < first_s):
-                first_s, first_e = res.first_fail_sample, res.first_fail_elem
-            if fail_fast and failed:
-                break
+        done = 0
+        try:
+            for i in range(nb):
+                j = first_batch + i * batch_stride
+                self.target.fill(stream=j)
+                self._check_run(lib.sip_run_async(self.module.handle, None, ctypes.byref(self.launch_ref)))
+                self._check_run(lib.sip_run_async(self.module.handle, pp, ctypes.byref(self.launch_cand)))
+                self.ctx.check(lib.sip_verify_compare(
+                    acc, ctypes.c_void_p(self.out_ref.data_ptr()), ctypes.c_void_p(self.out_cand.data_ptr()),
+                    self.out_ref.numel(), 0, self.atol, self.rtol, j * self.batch))
+                done += self.batch
+                if (i + 1) % check_every == 0 or i == nb - 1:
+                    self._check_run(lib.sip_verify_result(acc, ctypes.byref(res)))
+                    if fail_fast and res.failed_samples:
+                        break
+        finally:
+            lib.sip_verify_close(acc)
         dt = time.perf_counter() - t0
-        nbytes = 2 * 2 * self.out_ref.numel() * (i + 1)
-        return VerifyResult(done, passed, failed, first_s, first_e, bitdiff, mism, maxerr, dt, nbytes)
+        nbytes = 2 * 2 * self.elems_per_sample * done
+        failed = int(res.failed_samples)
+        return VerifyResult(done, done - failed, failed, int(res.first_fail_sample), int(res.first_fail_elem),
+                            int(res.bitdiff_elems), int(res.mismatched_elems), float(res.max_abs_err), dt, nbytes)
+
+    def _check_run(self, rc: int) -> None:
+        if rc == SIP_E_MEASURE:
+            raise MeasurementFailed(self.ctx.lib.sip_last_error(self.ctx.handle).decode(errors="replace"))
+        self.ctx.check(rc)

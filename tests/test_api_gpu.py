@@ -66,3 +66,32 @@ def test_estimator_fit_transform():
     assert parse_kernel(out).schedule[0].base_mnemonic == "LDG"
     with pytest.raises(ValueError):
         t.transform("MOV R0, RZ ;\n")
+
+
+def test_b200_external_adapter(tmp_path):
+    """The reference's external protocol priced on the B200: ExternalCommandBackend
+    (backends.py:73-116) spawns `sip measure`, which prints one {"time_ms": x} line."""
+    import sys
+
+    from paper_2403_16863_b200 import serialize_kernel
+    from paper_2403_16863_b200.backends import ExternalCommandBackend, MeasurementFailed
+    from paper_2403_16863_b200.cubin import render_listing
+    from paper_2403_16863_b200.ir import Kernel
+    from paper_2403_16863_b200.targets import TARGET_DIR
+
+    listing = render_listing((TARGET_DIR / "gemm_lrelu.cubin").read_bytes(), "gemm_lrelu_f16")
+    cmd = (f"{sys.executable} -m paper_2403_16863_b200 measure --target gemm "
+           "--shape M=512,N=512,K=2048 --reps 3 {schedule_file}")
+    from pathlib import Path
+
+    be = ExternalCommandBackend(cmd, timeout_s=300, workdir=str(Path(__file__).resolve().parents[1]))
+    s = be.measure(listing.kernel, reps=1)
+    assert s.unit == "ms" and 0.0 < s.value < 5.0
+    # a schedule that is not a permutation of the cubin is a measurement failure
+    sched = list(listing.kernel.schedule)
+    bad = Kernel(name="bad", schedule=tuple(sched[:-1] + [sched[0]]))
+    with pytest.raises(MeasurementFailed):
+        be.measure(bad, reps=1)
+    f = tmp_path / "x.sass"
+    f.write_text(serialize_kernel(listing.kernel))
+    assert main(["measure", str(f), "--shape", "M=512,N=512,K=2048", "--reps", "2"]) == 0

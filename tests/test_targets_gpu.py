@@ -146,7 +146,17 @@ def test_gemm_verifier_detects_a_broken_schedule():
     data = reads_writes(seq[s])[0]
     # the last pack whose result the first store reads
     f = max(i for i in range(s) if names[i] == "F2FP" and reads_writes(seq[i])[1] & data)
-    perm = np.arange(L.n, dtype=np.uint16)
-    perm[f], perm[s] = perm[s], perm[f]
+    # sink that pack below the store (the store's address computation stays in place,
+    # so the store writes stale data instead of faulting)
+    order = [i for i in range(L.n) if i != f]
+    order.insert(order.index(s) + 1, f)
+    perm = np.array(order, dtype=np.uint16)
     res = ver.run(perm, 32)
     assert not res.ok and res.first_fail_sample == 0
+    assert res.samples == 32 and res.failed == 32
+    # rank-strided batches (rank 1 of 2: batches 1, 3, 5): the first failure is a
+    # global sample index; fail_fast stops at the first check
+    res = ver.run(perm, 48, first_batch=1, batch_stride=2, fail_fast=True, check_every=1)
+    assert res.first_fail_sample == 16 and res.samples == 16 and res.failed == 16
+    ok = ver.run(np.arange(L.n, dtype=np.uint16), 48, first_batch=1, batch_stride=2)
+    assert ok.ok and ok.samples == 48 and ok.bitdiff_elems == 0 and ok.first_fail_sample == -1

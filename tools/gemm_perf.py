@@ -6,7 +6,7 @@ from paper_2403_16863_b200.targets import GemmTarget
 from paper_2403_16863_b200.evaluator import B200Backend
 from paper_2403_16863_b200.cubin import schedule_perm
 
-for (M, N, K) in [(4096, 4096, 4096), (8192, 8192, 8192)]:
+for (M, N, K) in [(4096, 4096, 4096), (8192, 8192, 8192), (2048, 2048, 2048), (512, 512, 2048)]:
     tgt = GemmTarget(M=M, N=N, K=K).allocate()
     be = B200Backend(tgt, flush_l2=True)
     ident = schedule_perm(be.kernel)

@@ -10,6 +10,12 @@ if which == "gemm":
     be = B200Backend(GemmTarget(M=4096, N=4096, K=4096).allocate())
     for _ in range(3):
         be.run_perm(None)
+elif which == "attn":
+    from paper_2403_16863_b200.attention import AttnTarget
+    from paper_2403_16863_b200.evaluator import B200Backend
+    be = B200Backend(AttnTarget(B=4, H=32, S=4096, D=128).allocate())
+    for _ in range(3):
+        be.run_perm(None)
 elif which == "engine":
     from bench import decoded_listing
     from paper_2403_16863_b200 import AnnealConfig
