@@ -55,15 +55,18 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--sim-chains", type=int, default=131072, help="engine chains per GPU")
-    ap.add_argument("--chains", type=int, default=8, help="hardware-priced chains per GPU")
-    ap.add_argument("--hw-steps", type=int, default=8, help="hardware search rounds")
+    ap.add_argument("--chains", type=int, default=16, help="hardware-priced chains per GPU")
+    ap.add_argument("--hw-steps", type=int, default=24, help="hardware search rounds")
+    ap.add_argument("--classes", default="extended", choices=["global", "extended"],
+                    help="hardware-phase candidate classes: the reference's (global) or the "
+                         "sm_100 extension (DESIGN.md s5b); the simulator headline always uses global")
     ap.add_argument("--epoch", type=int, default=8, help="rounds between global-best exchanges")
     ap.add_argument("--verify-samples", type=int, default=10_000_000,
                     help="samples per accepted (champion) schedule, sharded over ranks")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-attn", action="store_true")
-    ap.add_argument("--attn-steps", type=int, default=3, help="attention hardware search rounds")
+    ap.add_argument("--attn-steps", type=int, default=8, help="attention hardware search rounds")
     return ap.parse_args()
 
 
@@ -258,7 +261,8 @@ def hardware_phase(kind, listing, local, rank, world, dist, args, rounds):
     tgt = make_target(kind, device=local, **shape).allocate()
     be = B200Backend(tgt, listing, device=local, warmup=2, flush_l2=True)
     n = be.listing.n
-    hcfg = AnnealConfig(seed=0, t_max=0.02, t_min=0.0005, cooling=1.02, measure_reps=5)
+    hcfg = AnnealConfig(seed=0, t_max=0.02, t_min=0.0005, cooling=1.02, measure_reps=5,
+                        candidate_classes=args.classes)
     hs = HardwareSearch(be, hcfg, args.chains, epoch=args.epoch, dist=dist)
     hs.step()
     be.kernel_ms.clear()
@@ -299,6 +303,7 @@ def hardware_phase(kind, listing, local, rank, world, dist, args, rounds):
                 else "fallback 1590 TFLOP/s"}
     floor_ms = (2 if be.paired else 1) * (be.warmup + hcfg.measure_reps) * avg_ms
     hw = {"candidates_per_s": h_eval / (h_ms / 1e3), "rounds": rounds, "chains_per_gpu": args.chains,
+          "candidate_classes": args.classes, "candidates_in_listing": int(hs.dk.k),
           "proposals": rounds * args.chains * world, "priced": int(h_eval),
           "evaluator_roofline_candidates_per_s": world * 1e3 / floor_ms,
           "device_busy_frac": (h_eval / (h_ms / 1e3)) / (world * 1e3 / floor_ms),
@@ -309,10 +314,18 @@ def hardware_phase(kind, listing, local, rank, world, dist, args, rounds):
     if dist:
         hs.exchange()
         res = hs.result()
+    # acceptance: the best schedule that survives a fail-fast verification screen (SIP
+    # rejects candidates whose outputs differ); the survivor then gets the full run below
+    ver = Verifier(kind, device=local)
+    acc_e, acc_perm, rejected = hs.verified_best(ver)
+    if dist:  # every rank screened the same exchanged ranking; rank 0's choice wins
+        bt = torch.from_numpy(acc_perm.astype(np.int32)).cuda()
+        dist.broadcast(bt, 0)
+        acc_perm = bt.cpu().numpy().astype(np.uint16)
     tuned = verify = None
     if rank == 0:
         ident = np.arange(n, dtype=np.uint16)
-        best = res["best_perm"]
+        best = acc_perm
         ratio, raw = be.ratio(best, 45)  # paired: nvcc and best schedules alternate in one graph
         t_nvcc = be._measure_single(ident, 15).value
         t_best = t_nvcc * ratio
@@ -321,16 +334,13 @@ def hardware_phase(kind, listing, local, rank, world, dist, args, rounds):
                  "speedup_iqr": [1.0 / q3, 1.0 / q1], "pairs": 45,
                  "nvcc_tflops": tgt.flops / t_nvcc / 1e9, "best_tflops": tgt.flops / t_best / 1e9,
                  "instructions_moved": int((best != ident).sum()),
-                 "search_best_energy": res["best_energy"],
+                 "search_best_energy": res["best_energy"], "accepted_energy": acc_e,
+                 "rejected_by_verification": [{"energy": e, "first_failing_sample": v.first_fail_sample,
+                                               "max_abs_err": v.max_abs_err} for e, v in rejected],
                  "paper_speedup": 1.1227 if kind == "gemm" else 1.062}
     # every rank verifies its share of the samples (batches rank, rank+world, ...) of the
     # same champion; (passed, failed) sum and the first failing sample is the min over ranks
-    best = res["best_perm"]
-    if dist:
-        bt = torch.from_numpy(best.astype(np.int32)).cuda()
-        dist.broadcast(bt, 0)
-        best = bt.cpu().numpy().astype(np.uint16)
-    ver = Verifier(kind, device=local)
+    best = acc_perm
     per_rank = -(-args.verify_samples // (world * ver.batch)) * ver.batch
     vr = ver.run(best, per_rank, first_batch=rank, batch_stride=world)
     tot = allreduce(dist, [vr.samples, vr.passed, vr.failed, vr.bitdiff_elems, vr.compared_bytes], SUM)

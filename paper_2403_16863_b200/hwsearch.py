@@ -95,6 +95,34 @@ class HardwareSearch:
         be, _, _, sched = exchange_best(self.dist, e, seed, sched, torch.device("cuda", self.be.device))
         self.chains.adopt(sched, be, be * self.t0)
 
+    def ranked(self):
+        """Distinct per-chain best schedules, best (energy, seed) first."""
+        hist, best, cur, summ = self.chains.result()
+        order = sorted(range(self.C), key=lambda c: (float(summ["best_energy"][c]), self.seeds[c]))
+        seen, out = set(), []
+        for c in order:
+            key = best[c].tobytes()
+            if key not in seen:
+                seen.add(key)
+                out.append((float(summ["best_energy"][c]), self.seeds[c], best[c]))
+        return out
+
+    def verified_best(self, verifier, screen: int = 100_000, limit: int = 8):
+        """SIP's acceptance rule (difftest.run_tests fail_fast): walk the
+        ranked schedules and keep the first that passes a fail-fast screen of `screen`
+        samples; schedules that fail are rejected.  Falls back to the nvcc schedule.
+        Returns (energy, schedule, rejected list of (energy, VerifyResult))."""
+        rejected = []
+        ident = np.arange(self.dk.n, dtype=np.uint16)
+        for e, _, sched in self.ranked()[:limit]:
+            if e >= 1.0 or np.array_equal(sched, ident):
+                break
+            vr = verifier.run(sched, screen, fail_fast=True, check_every=8)
+            if vr.ok:
+                return e, sched, rejected
+            rejected.append((e, vr))
+        return 1.0, ident, rejected
+
     def result(self):
         e, seed, sched, hist, summ = self.local_best()
         priced = int(np.count_nonzero(hist["status"] <= ST_PRICED))

@@ -127,7 +127,7 @@ def test_attention_listing_and_verifier():
     L = render_listing(*ver.target.cubin())
     names = {ins.base_mnemonic for ins in L.kernel.schedule}
     assert {"UTCHMMA", "UTMALDG", "LDTM", "STG", "MUFU"} <= names
-    assert len(candidates(L.kernel)) >= 8
+    assert len(candidates(L.kernel)) >= 4  # the epilogue STG.128s (+ the generic TMEM-slot load)
     res = ver.run(np.arange(L.n, dtype=np.uint16), 128)
     assert res.ok and res.bitdiff_elems == 0 and res.samples == 128
 
@@ -160,3 +160,31 @@ def test_gemm_verifier_detects_a_broken_schedule():
     assert res.first_fail_sample == 16 and res.samples == 16 and res.failed == 16
     ok = ver.run(np.arange(L.n, dtype=np.uint16), 48, first_batch=1, batch_stride=2)
     assert ok.ok and ok.samples == 48 and ok.bitdiff_elems == 0 and ok.first_fail_sample == -1
+
+
+@pytest.mark.parametrize("kind", ["gemm", "attn"])
+def test_every_hw_safe_single_swap_verifies(kind):
+    """Legality audit on the hardware: every single adjacent swap of the nvcc schedule
+    that hw_safe admits under the extended classes must leave the outputs bit-identical
+    (this caught carry-out predicates, fixed-latency WAR on guards and the long
+    predicate latency)."""
+    from paper_2403_16863_b200.tables import movable_in
+    from paper_2403_16863_b200.targets import make_target
+    from paper_2403_16863_b200.verify import Verifier
+
+    shape = dict(M=512, N=512, K=512) if kind == "gemm" else dict(B=1, H=2, S=512)
+    be = B200Backend(make_target(kind, **shape).allocate(), paired=False)
+    seq = be.kernel.schedule
+    n = len(seq)
+    dk = be.ctx.kernel(be.tables_for(be.kernel, "extended"))
+    ident = np.arange(n, dtype=np.uint16)
+    los = [lo for lo in range(n - 1)
+           if movable_in(seq[lo], "extended") or movable_in(seq[lo + 1], "extended")]
+    legal = dk.legality(np.tile(ident, (len(los), 1)), los, hw_safe=True, min_fixed=be.min_fixed)
+    assert legal.sum() > 0
+    ver = Verifier(kind, batch=32)
+    for lo in np.asarray(los)[legal.astype(bool)]:
+        perm = ident.copy()
+        perm[lo], perm[lo + 1] = perm[lo + 1], perm[lo]
+        vr = ver.run(perm, 64, fail_fast=True, check_every=1)
+        assert vr.ok and vr.bitdiff_elems == 0, (int(lo), str(seq[lo].source_text), str(seq[lo + 1].source_text))

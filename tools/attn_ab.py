@@ -7,14 +7,20 @@ from paper_2403_16863_b200.cubin import Module, schedule_perm
 from paper_2403_16863_b200.engine import get_context
 import ctypes, numpy as np
 variants = {"current": "paper_2403_16863_b200/targets/attn_fwd.cubin"}
+threads = {}
 for a in sys.argv[1:]:
-    variants[a.split("/")[-1]] = a
+    path, _, nt = a.partition("@")  # path@384: launch with 384 threads (older 1-warp-per-row layout)
+    variants[path.split("/")[-1]] = path
+    if nt:
+        threads[path.split("/")[-1]] = int(nt)
 tgt = AttnTarget(B=4, H=32, S=4096).allocate()
 ctx = get_context()
 mods = {k: Module(open(v, 'rb').read(), "attn_fwd_f16", ctx=ctx) for k, v in variants.items()}
 for rnd in range(3):
     for k, m in mods.items():
         lp, params = tgt.launch()
+        if k in threads:
+            lp.block[0] = threads[k]
         med = ctypes.c_double(); raw = np.zeros(10)
         ctx.check(ctx.lib.sip_measure(m.handle, None, ctypes.byref(lp), 2, 10, 0, ctypes.byref(med),
                                       raw.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))

@@ -6,7 +6,8 @@ from paper_2403_16863_b200.attention import AttnTarget
 from paper_2403_16863_b200.evaluator import B200Backend
 from paper_2403_16863_b200.cubin import schedule_perm
 
-for cub in ["attn_fwd.cubin"]:
+cubs = ["attn_fwd.cubin"] + sys.argv[1:]
+for cub in cubs:
     tgt = AttnTarget(B=1, H=2, S=512, cubin_file=cub).allocate()
     be = B200Backend(tgt)
     be.run_perm(None)
