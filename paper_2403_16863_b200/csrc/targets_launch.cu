@@ -101,9 +101,9 @@ int sip_target_attn_launch(sip_ctx* ctx, const void* Q, const void* K, const voi
   launch->block[0] = 384;  // warpgroup 0 (TMA, MMA) + one softmax warpgroup per tile (SIP_SPLIT 1)
   launch->block[1] = launch->block[2] = 1;
   launch->cluster[0] = launch->cluster[1] = launch->cluster[2] = 1;
-  // Q 2 tiles, K and V 2 stages each; 1 KB alignment slack; 128 B of mbarriers; 4 KB of
-  // row max / sum exchange between the two softmax warps of a row
-  launch->smem_bytes = 6 * 128 * 128 * 2 + 1024 + 128 + 4096;
+  // Q 2 tiles, K and V 2 stages each; 1 KB alignment slack; 144 B of mbarriers (+ the
+  // TMEM slot); 4 KB of row max / sum exchange (used when the softmax splits a row)
+  launch->smem_bytes = 6 * 128 * 128 * 2 + 1024 + 144 + 4096;
   launch->params = params;
   launch->param_offsets = kAttnOffsets;
   launch->nparams = 9;

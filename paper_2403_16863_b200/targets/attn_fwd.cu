@@ -132,10 +132,10 @@ attn_fwd_f16(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CU
   uint64_t* v_full = bars + 5;        // [2]
   uint64_t* v_empty = bars + 7;       // [2]
   uint64_t* s_full = bars + 9;        // [tile]
-  uint64_t* p_full = bars + 11;       // [tile]
-  uint64_t* o_done = bars + 13;       // [tile]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
-  float* xch = reinterpret_cast<float*>(bars + 16);  // [tile][parity][SPLIT][128] row maxima / sums
+  uint64_t* p_full = bars + 11;       // [tile][half]: P_X keys 0-63 / 64-127 in TMEM
+  uint64_t* o_done = bars + 15;       // [tile]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  float* xch = reinterpret_cast<float*>(bars + 18);  // [tile][parity][SPLIT][128] row maxima / sums
 
   const int warp = warp_id();
   const int lane = threadIdx.x & 31;
@@ -153,7 +153,8 @@ attn_fwd_f16(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CU
       mbar_init(&v_full[i], 1);
       mbar_init(&v_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 4 * SPLIT);
+      mbar_init(&p_full[2 * i], 4);  // the 4 warps (one per lane quarter) owning that half
+      mbar_init(&p_full[2 * i + 1], 4);
       mbar_init(&o_done[i], 1);
     }
     mbar_fence_init();
@@ -204,12 +205,12 @@ attn_fwd_f16(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CU
                 desc_sw128(k0 + (kk >> 2) * HALF + (kk & 3) * 32), IDESC_QK, kk != 0);
       mma_commit(&s_full[x]);
     };
-    auto pv = [&](int x, int t) {  // O_X += P_X V[t]; P_X: fp16 pairs in S_X's columns 0..63
+    auto pv = [&](int x, int t, int h) {  // O_X += P_X V[t], keys 64h..64h+63 (P columns 32h..)
       const uint32_t v0 = smem_u32(sV + (t & 1) * TILE_BYTES);
 #pragma unroll
-      for (int kk = 0; kk < BN / 16; ++kk)
+      for (int kk = 4 * h; kk < 4 * h + 4; ++kk)
         mma_f16_ts(tO(x), tS(x) + kk * 8, desc_v(v0 + kk * 16 * 128), IDESC_PV, (t | kk) != 0);
-      mma_commit(&o_done[x]);
+      if (h == 1) mma_commit(&o_done[x]);
     };
     mbar_wait(q_full, 0);
     mbar_wait(&k_full[0], 0);
@@ -227,10 +228,15 @@ attn_fwd_f16(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CU
       mbar_wait(&v_full[st], ph);
       if (more) mbar_wait(&k_full[st ^ 1], ((t + 1) >> 1) & 1);
       for (int x = 0; x < 2; ++x) {
-        mbar_wait(&p_full[x], t & 1);  // softmax X wrote P_X(t) (and rescaled O_X)
+        // the first half of PV_X(t) starts while softmax X still exponentiates keys 64-127
+        mbar_wait(&p_full[2 * x], t & 1);  // keys 0-63 of P_X(t) written (O_X rescaled)
+        tc_fence_after();
+        if (elect_one()) pv(x, t, 0);
+        __syncwarp();
+        mbar_wait(&p_full[2 * x + 1], t & 1);
         tc_fence_after();
         if (elect_one()) {
-          pv(x, t);
+          pv(x, t, 1);
           if (more) qk(x, t + 1);  // in-order after PV_X(t): safe to overwrite S_X / P_X
           if (x == 1) {
             mma_commit(&v_empty[st]);
@@ -300,29 +306,8 @@ attn_fwd_f16(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CU
         alpha = exp2f(m_used - m_new);  // 0 on the first tile
         m_used = m_new;
       }
-      const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m_used, -m_used);
-      float2 rq[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};  // independent partial sums
-#pragma unroll
-      for (int c = 0; c < CW / 64; ++c) {  // P -> tensor memory, 32 packed columns at a time
-        uint32_t pk[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float2 z = ffma2(make_float2(s[c * 64 + 2 * j], s[c * 64 + 2 * j + 1]), sc2, nm2);
-          float2 e;
-          if ((j & 7) < SIP_POLY8) {
-            e = ex2_poly2(z);
-          } else {
-            e.x = ex2_mufu(z.x);
-            e.y = ex2_mufu(z.y);
-          }
-          pk[j] = pack_half2(e.x, e.y);
-          rq[j & 3] = fadd2(rq[j & 3], e);
-        }
-        tmem_st32(tS(x) + lane_off + hh * (CW / 2) + c * 32, pk);
-      }
-      const float2 r2 = fadd2(fadd2(rq[0], rq[1]), fadd2(rq[2], rq[3]));
-      l = l * alpha + (r2.x + r2.y);  // this part's share of the row sum
-      // rescale O_X (rare): PV_X(t-1) must be complete; PV_X(t) waits for p_full below
+      // rescale O_X (rare) before any P of this step is published: PV_X(t-1) must be
+      // complete; the first half of PV_X(t) waits for p_full below
       if (__any_sync(0xffffffffu, grow && t > 0)) {
         mbar_wait(&o_done[x], (t - 1) & 1);
         tc_fence_after();
@@ -338,10 +323,33 @@ attn_fwd_f16(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CU
           }
         }
       }
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[x]);
+      const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m_used, -m_used);
+      float2 rq[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};  // independent partial sums
+#pragma unroll
+      for (int c = 0; c < CW / 64; ++c) {  // P -> tensor memory, 32 packed columns (64 keys) at a time
+        uint32_t pk[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float2 z = ffma2(make_float2(s[c * 64 + 2 * j], s[c * 64 + 2 * j + 1]), sc2, nm2);
+          float2 e;
+          if ((j & 7) < SIP_POLY8) {
+            e = ex2_poly2(z);
+          } else {
+            e.x = ex2_mufu(z.x);
+            e.y = ex2_mufu(z.y);
+          }
+          pk[j] = pack_half2(e.x, e.y);
+          rq[j & 3] = fadd2(rq[j & 3], e);
+        }
+        tmem_st32(tS(x) + lane_off + hh * (CW / 2) + c * 32, pk);
+        // publish this half of P_X(t) (and, with it, any O rescale above)
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[2 * x + hh * (CW / 64) + c]);
+      }
+      const float2 r2 = fadd2(fadd2(rq[0], rq[1]), fadd2(rq[2], rq[3]));
+      l = l * alpha + (r2.x + r2.y);  // this part's share of the row sum
     }
     if (SPLIT > 1) {  // full row sum from the parts (slot parity T&1 is free: last use was T-2)
       float* slot = xch + ((x * 2 + (T & 1)) * SPLIT) * 128;
