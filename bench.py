@@ -363,6 +363,10 @@ def main() -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: SIP_SHARE_DEVICE=1 runs every rank on cuda:0 (with SIP_DIST_BACKEND=gloo) so
+    # the multi-rank path can be exercised on a one-GPU box; never used for reported numbers
+    if os.environ.get("SIP_SHARE_DEVICE") == "1":
+        local = 0
     if args.impl == "reference":
         run_reference(args, rank)
         return
@@ -375,7 +379,11 @@ def main() -> None:
     if world > 1:
         import torch.distributed as td
 
-        td.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("SIP_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            td.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            td.init_process_group(backend)
         dist = td
     os.environ["SIP_DEVICE"] = str(local)
     MAX = dist.ReduceOp.MAX if dist else None
