@@ -243,7 +243,7 @@ def allreduce(dist, vals, op):
     return t.tolist()
 
 
-def hardware_phase(kind, listing, local, rank, world, dist, args, rounds):
+def hardware_phase(kind, listing, local, rank, world, dist, args, rounds, shape=None):
     """Hardware-priced search on one tuning target: rate, roofline, tuned vs nvcc, verification."""
     import numpy as np
     import torch
@@ -257,7 +257,7 @@ def hardware_phase(kind, listing, local, rank, world, dist, args, rounds):
     MAX = dist.ReduceOp.MAX if dist else None
     SUM = dist.ReduceOp.SUM if dist else None
     MIN = dist.ReduceOp.MIN if dist else None
-    shape = SHAPE if kind == "gemm" else ATTN_SHAPE
+    shape = shape or (SHAPE if kind == "gemm" else ATTN_SHAPE)
     tgt = make_target(kind, device=local, **shape).allocate()
     be = B200Backend(tgt, listing, device=local, warmup=2, flush_l2=True)
     n = be.listing.n

@@ -75,3 +75,25 @@ def test_million_sample_verdict_throughput():
     dt = time.perf_counter() - t0
     assert v.ok and v.passed == 1_000_000
     print(f"1M samples in {dt:.2f}s = {1e6 / dt:.0f} samples/s")
+
+
+def test_fill_normal_statistics_and_streams():
+    """sip_fill_normal: N(0, sigma^2) fp16, reproducible per (seed, stream), streams differ."""
+    import ctypes
+
+    import torch
+
+    from paper_2403_16863_b200.engine import get_context
+
+    ctx = get_context()
+    n = 1 << 22
+    a, b, c = (torch.empty(n, dtype=torch.float16, device="cuda") for _ in range(3))
+    for t, stream in ((a, 5), (b, 5), (c, 6)):
+        ctx.check(ctx.lib.sip_fill_normal(ctx.handle, ctypes.c_void_p(t.data_ptr()), n, 0, 11, stream, 0.5))
+    torch.cuda.synchronize()
+    assert torch.equal(a, b) and not torch.equal(a, c)
+    x = a.float()
+    assert abs(x.mean().item()) < 2e-3 and abs(x.std().item() - 0.5) < 5e-3
+    assert x.abs().max().item() < 0.5 * 4.8  # 16-bit Box-Muller bound
+    frac = (x.abs() < 0.5).float().mean().item()  # P(|z| < 1) = 0.6827
+    assert abs(frac - 0.6827) < 3e-3
