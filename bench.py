@@ -412,15 +412,16 @@ def main() -> None:
     best = {"e": 1.0, "perm": None}
 
     def epoch(ep: int):
-        seeds = np.arange(C, dtype=np.int64) + (ep * world + rank) * C
-        _, summ, champ, _ = dk.anneal_epoch(seeds, temps, start=best["perm"], with_history=False)
-        i = int(np.lexsort((seeds, summ["best_energy"]))[0])
-        e_mine = float(summ["best_energy"][i])
+        # chains seeded (ep*world + rank)*C + c on the device; the champion (best energy,
+        # then seed) and the counters are reduced there too, so a step moves ~2 KB
+        res, champ = dk.anneal_epoch_reduced((ep * world + rank) * C, C, temps, start=best["perm"])
+        e_mine = float(res["best_energy"])
         if dist:  # NCCL allgather of (energy, seed, rank); owner broadcasts its champion
-            e_mine, _, _, champ = exchange_best(dist, e_mine, int(seeds[i]), champ, torch.device("cuda", local))
+            e_mine, _, _, champ = exchange_best(dist, e_mine, int(res["best_seed"]), champ,
+                                                torch.device("cuda", local))
         if e_mine < best["e"]:
             best["e"], best["perm"] = e_mine, champ
-        return int(summ["priced"].sum()), int(summ["replayed"].sum()), int(summ["ambiguous"].sum())
+        return int(res["priced"]), int(res["replayed"]), int(res["ambiguous"])
 
     for w in range(args.warmup):
         epoch(w)

@@ -99,6 +99,18 @@ typedef struct {
   int32_t pad;
 } sip_chain_summary;
 
+/* One epoch of a sharded search, reduced on the device (bench / run_search
+ * sharding): the champion chain under driver.py:81-85's ranking and the sums. */
+typedef struct {
+  int32_t champion_chain;
+  int32_t pad;
+  double best_energy;
+  int64_t best_seed;
+  int64_t priced;
+  int64_t replayed;
+  int64_t ambiguous;
+} sip_epoch_result;
+
 /* ---- context -------------------------------------------------------- */
 const char* sip_version(void);
 int sip_device_count(int* count);
@@ -141,6 +153,10 @@ int sip_anneal_ex(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds
  * summaries come back.  Results are pulled per chain range on demand (the
  * public API's AnnealState materialises lazily).  A result set must be
  * destroyed before its sip_kernel.                                       */
+/* fused chains with consecutive seeds seed_base + c (generated on the device),
+ * reduced to one sip_epoch_result; `champion` receives that chain's best schedule */
+int sip_anneal_epoch(sip_kernel* k, const sip_anneal_cfg* cfg, int64_t seed_base, int32_t chains,
+                     const uint16_t* start, sip_epoch_result* result, uint16_t* champion);
 int sip_anneal_keep(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds, int32_t chains,
                     const uint16_t* start, sip_chain_summary* summary, sip_results** out);
 int sip_results_fetch(sip_results* r, int32_t first, int32_t count, sip_record* history,

@@ -71,4 +71,5 @@ struct sip_kernel {
   int64_t baseline = 0;         // identity-schedule scoreboard total
   struct sip_chains* ws = nullptr;  // reusable chain workspace of sip_anneal_ex
   uint32_t* d_base = nullptr;   // MT19937 init_genrand(19650218) state
+  void* d_epoch = nullptr;      // sip_epoch_result of the last sip_anneal_epoch
 };

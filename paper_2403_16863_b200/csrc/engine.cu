@@ -199,17 +199,19 @@ struct Sb {
 #pragma unroll
     for (int b = 0; b < 6; ++b) clr[b] = 0;
   }
+  // m.x = packed ctrl (wait mask in bits 0-5); m.y = latency (bits 0-15) | mask of
+  // the barriers this instruction sets, rd or wr (bits 16-21) -- precomputed on
+  // the host so a step is two masked 6-way updates and no field decoding
   __device__ __forceinline__ void step(uint2 m) {
-    uint32_t c = m.x;
+    const uint32_t c = m.x, setm = m.y >> 16;
     int issue = ptr;
 #pragma unroll
     for (int b = 0; b < 6; ++b)
       if ((c >> b) & 1u) issue = max(issue, clr[b]);
-    int done = issue + (int)m.y;
-    uint32_t rd = c_rd(c), wr = c_wr(c);
+    const int done = issue + (int)(m.y & 0xFFFFu);
 #pragma unroll
     for (int b = 0; b < 6; ++b)
-      if (rd == (uint32_t)b || wr == (uint32_t)b) clr[b] = done;
+      if ((setm >> b) & 1u) clr[b] = done;
     fin = max(fin, done);
     ptr = issue + (int)c_adv(c);
   }
@@ -247,6 +249,8 @@ struct Chains {
   int nck = 0;                      // scoreboard checkpoints per chain (every CK positions)
   int32_t* ckpt = nullptr;          // [nck][8][C] state of the current schedule
   int32_t* ckpt2 = nullptr;         // [nck][8][C] state of the candidate being priced
+  int32_t* ck0 = nullptr;           // [nck][8] + total: checkpoints of the start schedule
+  uint16_t* acclog = nullptr;       // [budget][C] lo of every accepted swap (fused kernel)
   int64_t* replayed = nullptr;      // [C] scoreboard steps executed (instrumentation)
   int32_t* priced = nullptr;        // [C] priced iterations
 };
@@ -327,16 +331,25 @@ __device__ Staged stage_tables(const KernelDev& d, bool use_smem) {
   return {m, g};
 }
 
-__device__ void chain_init(const KernelDev& d, const Chains& s, int c, const uint32_t* base,
-                           MtRef& mt) {
+__device__ void chain_init(const KernelDev& d, const int16_t* gid, const Chains& s, int c,
+                           const uint32_t* base, MtRef& mt) {
+  // rows written 8 positions per 16-byte store; candidate lookups from the staged table
+  uint4* srow = reinterpret_cast<uint4*>(s.sched + (size_t)c * s.ns);
+  uint4* brow = reinterpret_cast<uint4*>(s.best + (size_t)c * s.ns);
   int j = 0;
-  for (int p = 0; p < s.n; ++p) {
-    uint16_t x = s.start ? s.start[p] : (uint16_t)p;
-    s.sched[(size_t)c * s.ns + p] = x;
-    s.best[(size_t)c * s.ns + p] = x;
-    if (d.gid[x] >= 0) s.cpos[(size_t)(j++) * s.C + c] = (uint16_t)p;
+  for (int q = 0; q < s.ns / 8; ++q) {
+    uint16_t x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int p = q * 8 + i;
+      x[i] = p < s.n ? (s.start ? s.start[p] : (uint16_t)p) : (uint16_t)0;
+      if (p < s.n && gid[x[i]] >= 0) s.cpos[(size_t)(j++) * s.C + c] = (uint16_t)p;
+    }
+    const uint4 v = make_uint4(x[0] | ((uint32_t)x[1] << 16), x[2] | ((uint32_t)x[3] << 16),
+                               x[4] | ((uint32_t)x[5] << 16), x[6] | ((uint32_t)x[7] << 16));
+    srow[q] = v;
+    brow[q] = v;
   }
-  for (int p = s.n; p < s.ns; ++p) s.sched[(size_t)c * s.ns + p] = s.best[(size_t)c * s.ns + p] = 0;
   uint32_t key[2];
   int klen = mt_key_from_int(s.seeds[c], key);
   mt_init_by_array(mt, base, key, klen);
@@ -346,12 +359,19 @@ __device__ void chain_init(const KernelDev& d, const Chains& s, int c, const uin
 // The state before every CK-th position of the chain's current schedule is
 // kept (ptr, fin, 6 barrier clocks).  A candidate that swaps (lo, lo+1)
 // replays from the checkpoint below lo only, and stops as soon as its state
-// equals the current schedule's checkpoint further down: barrier clocks are
-// compared as max(clock, ptr), since a clock at or below the issue pointer
-// can never delay an issue again.  From that point both schedules issue
-// identically, so the candidate's total is the current total -- the replay
-// is exact, not an estimate (checked bit for bit against the oracle).
-constexpr int CK = 32;
+// equals the current schedule's checkpoint further down *up to a constant
+// shift delta*.  The recurrence (machine.py:116-161) is built from max and
+// +constant only, so states that differ by delta in every field evolve
+// identically apart from that shift, and the candidate's total is the current
+// total + delta.  Fields are compared as max(field, ptr): a barrier clock or
+// finish time at or below the issue pointer can never affect an issue or the
+// total again.  The replay is exact, not an estimate (checked bit for bit
+// against the oracle); the shift lets a swap that only moves everything later
+// by a cycle stop at the next checkpoint instead of replaying to the end.
+#ifndef SIP_CK
+#define SIP_CK 32
+#endif
+constexpr int CK = SIP_CK;
 
 __device__ __forceinline__ void ck_put(int32_t* base, int C, int c, int j, const Sb& st) {
   size_t i = (size_t)j * 8 * C + c;
@@ -369,13 +389,15 @@ __device__ __forceinline__ void ck_get(const int32_t* base, int C, int c, int j,
   for (int b = 0; b < 6; ++b) st.clr[b] = base[i + (size_t)(2 + b) * C];
 }
 
-__device__ __forceinline__ bool ck_same(const int32_t* base, int C, int c, int j, const Sb& st) {
+__device__ __forceinline__ bool ck_shift(const int32_t* base, int C, int c, int j, const Sb& st, int& delta) {
   size_t i = (size_t)j * 8 * C + c;
-  int ptr = base[i];
-  if (ptr != st.ptr || base[i + C] != st.fin) return false;
+  const int ptr = base[i];
+  const int dl = st.ptr - ptr;
+  if (max(st.fin, st.ptr) != max(base[i + C], ptr) + dl) return false;
 #pragma unroll
   for (int b = 0; b < 6; ++b)
-    if (max(base[i + (size_t)(2 + b) * C], ptr) != max(st.clr[b], ptr)) return false;
+    if (max(st.clr[b], st.ptr) != max(base[i + (size_t)(2 + b) * C], ptr) + dl) return false;
+  delta = dl;
   return true;
 }
 
@@ -399,22 +421,11 @@ __device__ __forceinline__ void replay_span(const uint2* meta, const uint16_t* r
   for (; p < p1; ++p) st.step(meta[row[p]]);
 }
 
-// full replay of the chain's current schedule, writing every checkpoint
-__device__ int ck_rebuild(const uint2* meta, const Chains& s, int c) {
-  Sb st;
-  st.reset();
-  const uint16_t* row = s.sched + (size_t)c * s.ns;
-  for (int j = 0; j < s.nck; ++j) {
-    ck_put(s.ckpt, s.C, c, j, st);
-    replay_span(meta, row, j * CK, min(s.n, (j + 1) * CK), st);
-  }
-  return st.total();
-}
-
 // total of the current schedule with (lo, lo+1) exchanged; jconv = first
-// checkpoint where the candidate rejoined the current trajectory (nck if never)
+// checkpoint where the candidate rejoined the current trajectory (nck if never),
+// delta = the constant shift it rejoined with
 __device__ int ck_price(const uint2* meta, const Chains& s, int c, int lo, int total_x, int& jconv,
-                        int64_t& steps) {
+                        int& delta, int64_t& steps) {
   const uint16_t* row = s.sched + (size_t)c * s.ns;
   const int C = s.C, n = s.n;
   int j0 = lo / CK;
@@ -428,11 +439,12 @@ __device__ int ck_price(const uint2* meta, const Chains& s, int c, int lo, int t
   int pb = min(n, ((p + CK - 1) / CK) * CK);
   replay_span(meta, row, p, pb, st);
   steps += (pb - j0 * CK);
+  delta = 0;
   for (p = pb; p < n; p += CK) {
     int j = p / CK;
-    if (ck_same(s.ckpt, C, c, j, st)) {
+    if (ck_shift(s.ckpt, C, c, j, st, delta)) {
       jconv = j;
-      return total_x;
+      return total_x + delta;
     }
     ck_put(s.ckpt2, C, c, j, st);
     int pe = min(n, p + CK);
@@ -443,13 +455,54 @@ __device__ int ck_price(const uint2* meta, const Chains& s, int c, int lo, int t
   return st.total();
 }
 
-// adopt the priced candidate's checkpoints (those past lo, before jconv)
-__device__ void ck_commit(const Chains& s, int c, int lo, int jconv) {
+// adopt the priced candidate's checkpoints: its own states past lo and before
+// jconv, the current ones shifted by delta from jconv on
+__device__ void ck_commit(const Chains& s, int c, int lo, int jconv, int delta) {
   for (int j = (lo + CK) / CK; j < jconv; ++j) {
     size_t i = (size_t)j * 8 * s.C + c;
 #pragma unroll
     for (int f = 0; f < 8; ++f) s.ckpt[i + (size_t)f * s.C] = s.ckpt2[i + (size_t)f * s.C];
   }
+  if (delta != 0)
+    for (int j = jconv; j < s.nck; ++j) {
+      size_t i = (size_t)j * 8 * s.C + c;
+#pragma unroll
+      for (int f = 0; f < 8; ++f) s.ckpt[i + (size_t)f * s.C] += delta;
+    }
+}
+
+// Every chain of a launch starts from the same schedule, so its checkpoints are
+// computed once (one thread) and copied by each chain instead of replayed n times.
+__global__ void start_ckpt_kernel(KernelDev d, Chains s) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  Sb st;
+  st.reset();
+  for (int j = 0; j < s.nck; ++j) {
+    int32_t* o = s.ck0 + (size_t)j * 8;
+    o[0] = st.ptr;
+    o[1] = st.fin;
+    for (int b = 0; b < 6; ++b) o[2 + b] = st.clr[b];
+    for (int p = j * CK; p < min(s.n, (j + 1) * CK); ++p)
+      st.step(d.meta[s.start ? s.start[p] : p]);
+  }
+  s.ck0[(size_t)s.nck * 8] = st.total();
+}
+
+__device__ int ck_copy_start(const Chains& s, int c) {
+  for (int j = 0; j < s.nck; ++j) {
+    const int4* src = reinterpret_cast<const int4*>(s.ck0 + (size_t)j * 8);
+    const int4 a = src[0], b = src[1];
+    size_t i = (size_t)j * 8 * s.C + c;
+    s.ckpt[i] = a.x;
+    s.ckpt[i + s.C] = a.y;
+    s.ckpt[i + 2 * (size_t)s.C] = a.z;
+    s.ckpt[i + 3 * (size_t)s.C] = a.w;
+    s.ckpt[i + 4 * (size_t)s.C] = b.x;
+    s.ckpt[i + 5 * (size_t)s.C] = b.y;
+    s.ckpt[i + 6 * (size_t)s.C] = b.z;
+    s.ckpt[i + 7 * (size_t)s.C] = b.w;
+  }
+  return s.ck0[(size_t)s.nck * 8];
 }
 
 // ---- fused simulator-energy annealing: whole chain in one launch ----------
@@ -460,12 +513,12 @@ __global__ void __launch_bounds__(128) anneal_fused_kernel(KernelDev d, Chains s
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= s.C) return;
   MtRef mt{s.mt + c, s.C, MT_N};
-  chain_init(d, s, c, mt_base, mt);
+  chain_init(d, tb.gid, s, c, mt_base, mt);
   const double t0 = t0_cycles;
-  int total_x = ck_rebuild(tb.meta, s, c);
-  int64_t steps = s.n;
+  int total_x = ck_copy_start(s, c);
+  int64_t steps = 0;  // scoreboard steps replayed by this chain (the start replay is shared)
   double e_x = (double)total_x / t0, e_best = e_x;
-  int best_iter = -1, amb = 0, priced = 0;
+  int best_iter = -1, amb = 0, priced = 0, nacc = 0, best_nacc = 0;
   for (int it = 0; it < s.budget; ++it) {
     int cand, dir, lo;
     int st = propose(d, tb.meta, tb.gid, s, c, mt, cand, dir, lo);
@@ -474,24 +527,38 @@ __global__ void __launch_bounds__(128) anneal_fused_kernel(KernelDev d, Chains s
       continue;
     }
     ++priced;
-    int jconv;
-    int tc = ck_price(tb.meta, s, c, lo, total_x, jconv, steps);
+    int jconv, delta;
+    int tc = ck_price(tb.meta, s, c, lo, total_x, jconv, delta, steps);
     double t = (double)tc;
     double e_c = t / t0;
     double de = e_c - e_x;
     bool acc = metropolis(de, s.temps[it], mt, amb);
     if (acc) {
       apply_swap(tb.gid, s, c, lo, cand, dir);
-      ck_commit(s, c, lo, jconv);
+      ck_commit(s, c, lo, jconv, delta);
+      s.acclog[(size_t)nacc * s.C + c] = (uint16_t)lo;
+      ++nacc;
       total_x = tc;
       e_x = e_c;
       if (de < 0 && e_c < e_best) {
         e_best = e_c;
         best_iter = it;
-        copy_best(s, c);
+        best_nacc = nacc;  // the best schedule = the current one after nacc accepted swaps
       }
     }
     record(s, c, it, acc ? SIP_ST_ACCEPTED : SIP_ST_PRICED, t, lo, cand, dir);
+  }
+  if (best_iter >= 0) {
+    // best row = current row with the swaps accepted after the best undone (adjacent
+    // swaps are their own inverse), instead of a full row copy at every new best
+    copy_best(s, c);
+    uint16_t* b = s.best + (size_t)c * s.ns;
+    for (int q = nacc - 1; q >= best_nacc; --q) {
+      const int l = s.acclog[(size_t)q * s.C + c];
+      const uint16_t t = b[l];
+      b[l] = b[l + 1];
+      b[l + 1] = t;
+    }
   }
   s.t0[c] = t0;
   s.e_x[c] = e_x;
@@ -509,7 +576,7 @@ __global__ void chains_init_kernel(KernelDev d, Chains s, const uint32_t* mt_bas
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= s.C) return;
   MtRef mt{s.mt + c, s.C, MT_N};
-  chain_init(d, s, c, mt_base, mt);
+  chain_init(d, d.gid, s, c, mt_base, mt);
   s.mti[c] = mt.mti;
   s.t0[c] = t0[c];
   s.e_x[c] = 1.0;
@@ -746,6 +813,8 @@ static int chains_alloc(sip_ctx* ctx, sip_kernel* k, const sip_anneal_cfg* cfg, 
   s.nck = (s.n + CK - 1) / CK;
   TRY(dalloc(ctx, &s.ckpt, (size_t)s.nck * 8 * C));
   TRY(dalloc(ctx, &s.ckpt2, (size_t)s.nck * 8 * C));
+  TRY(dalloc(ctx, &s.ck0, (size_t)s.nck * 8 + 4));
+  TRY(dalloc(ctx, &s.acclog, (size_t)std::max(s.budget, 1) * C));
   TRY(dalloc(ctx, &s.replayed, C));
   TRY(dalloc(ctx, &s.priced, C));
   SIP_CUDA(ctx, cudaMemsetAsync(s.replayed, 0, sizeof(int64_t) * C, ctx->stream));
@@ -755,7 +824,7 @@ static int chains_alloc(sip_ctx* ctx, sip_kernel* k, const sip_anneal_cfg* cfg, 
   SIP_CUDA(ctx, cudaMemsetAsync(s.hist, 0xFF, sizeof(sip_record) * (size_t)std::max(s.budget, 1) * C,
                                 ctx->stream));  // status 255 = iteration not run yet
   TRY(h2d(ctx, o->d_temps, cfg->temperature, (size_t)s.budget));
-  TRY(h2d(ctx, o->d_seeds, seeds, C));
+  if (seeds) TRY(h2d(ctx, o->d_seeds, seeds, C));
   s.temps = o->d_temps;
   s.seeds = o->d_seeds;
   return SIP_OK;
@@ -766,7 +835,7 @@ static void chains_free(sip_chains* o) {
   void* ptrs[] = {s.sched, s.best, s.cpos, s.mt, s.mti, s.t0, s.e_x, s.e_best, s.it,
                   s.best_iter, s.ambiguous, s.p_lo, s.p_cand, s.p_dir, s.hist, o->d_temps,
                   o->d_seeds, o->d_tcurr, o->d_status, o->d_lo, s.cand_out, o->d_adopt,
-                  s.ckpt, s.ckpt2, s.replayed, s.priced, o->d_start};
+                  s.ckpt, s.ckpt2, s.ck0, s.acclog, s.replayed, s.priced, o->d_start};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -838,7 +907,13 @@ int sip_kernel_create(sip_ctx* ctx, const sip_tables* t, sip_kernel** out) {
   std::vector<int16_t> gid(n, -1);
   std::vector<int32_t> gids;
   for (size_t i = 0; i < n; ++i) {
-    meta[i] = make_uint2(t->ctrl[i], t->lat[i]);
+    if (t->lat[i] > 0xFFFFu) {
+      delete k;
+      return sip::fail(ctx, SIP_E_ARG, "instruction latency above 65535 cycles");
+    }
+    const uint32_t c = t->ctrl[i], rd = c_rd(c), wr = c_wr(c);
+    const uint32_t setm = (rd < 6 ? 1u << rd : 0u) | (wr < 6 ? 1u << wr : 0u);
+    meta[i] = make_uint2(c, t->lat[i] | (setm << 16));
     if (t->ctrl[i] & CAND_BIT) {
       gid[i] = (int16_t)gids.size();
       gids.push_back((int32_t)i);
@@ -898,6 +973,7 @@ int sip_kernel_destroy(sip_kernel* k) {
     delete k->ws;
   }
   if (k->d_base) cudaFree(k->d_base);
+  if (k->d_epoch) cudaFree(k->d_epoch);
   KernelDev& d = k->d;
   void* ptrs[] = {d.meta, d.klass, d.reads, d.writes, d.refs, d.nrefs, d.cut,
                   d.pin,  d.gid,   d.gids,  d.e_after, d.e_before};
@@ -988,9 +1064,16 @@ done:
 }  // extern "C"
 
 // prepares the per-listing workspace and launches the fused kernel (no fetches)
+__global__ void seeds_fill_kernel(int64_t* seeds, int C, int64_t base) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < C) seeds[c] = base + c;
+}
+
+// seeds == nullptr: chain c gets seed_base + c (consecutive seeds, driver.py:73-79),
+// generated on the device instead of uploaded
 static int run_fused(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds, int32_t chains,
-                     const uint16_t* start, bool record_hist) {
-  if (!k || !cfg || !seeds || chains < 1 || cfg->budget < 0) return SIP_E_ARG;
+                     const uint16_t* start, bool record_hist, int64_t seed_base = 0) {
+  if (!k || !cfg || chains < 1 || cfg->budget < 0) return SIP_E_ARG;
   sip_ctx* ctx = k->ctx;
   if (k->d.k == 0) return fail(ctx, SIP_E_NOCAND, "no global-memory instructions to move");
   // chain state lives in a per-listing workspace reused across calls of the same shape
@@ -1016,9 +1099,10 @@ static int run_fused(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* se
     s.hw_safe = cfg->hw_safe;
     s.minfix = cfg->min_fixed_distance;
     TRY(h2d(ctx, k->ws->d_temps, cfg->temperature, (size_t)s.budget));
-    TRY(h2d(ctx, k->ws->d_seeds, seeds, (size_t)chains));
+    if (seeds) TRY(h2d(ctx, k->ws->d_seeds, seeds, (size_t)chains));
   }
   sip_chains& o = *k->ws;
+  if (!seeds) seeds_fill_kernel<<<(chains + 255) / 256, 256, 0, ctx->stream>>>(o.d_seeds, chains, seed_base);
   if (!k->d_base) {
     TRY(dalloc(ctx, &k->d_base, MT_N));
     TRY(h2d(ctx, k->d_base, mt_base_host().data(), MT_N));
@@ -1033,6 +1117,7 @@ static int run_fused(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* se
   size_t sm = smem_need(k->d);
   int use_smem = sm <= kSmemCap;
   if (use_smem) TRY(configure_smem(ctx, (const void*)anneal_fused_kernel, sm));
+  start_ckpt_kernel<<<1, 32, 0, ctx->stream>>>(k->d, o.s);
   anneal_fused_kernel<<<(chains + 127) / 128, 128, use_smem ? sm : 0, ctx->stream>>>(
       k->d, o.s, k->d_base, use_smem, (double)k->baseline);
   cudaError_t e = cudaGetLastError();
@@ -1067,6 +1152,82 @@ int sip_anneal_ex(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds
     SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     if (champion_chain) *champion_chain = w;
   }
+  return SIP_OK;
+}
+
+}  // extern "C"
+
+// One block reduces a launch to the epoch record: the champion under the reference's
+// ranking (best energy, then seed; driver.py:81-85) and the instrumentation sums.
+__global__ void __launch_bounds__(1024) epoch_reduce_kernel(Chains s, sip_epoch_result* out) {
+  __shared__ double se[1024];
+  __shared__ int64_t ss[1024], sp[1024], sr[1024], sa[1024];
+  __shared__ int sc[1024];
+  const int t = threadIdx.x;
+  double be = INFINITY;
+  int64_t bs = INT64_MAX, pri = 0, rep = 0, amb = 0;
+  int bc = -1;
+  for (int c = t; c < s.C; c += blockDim.x) {
+    const double e = s.e_best[c];
+    const int64_t sd = s.seeds[c];
+    if (e < be || (e == be && sd < bs)) {
+      be = e;
+      bs = sd;
+      bc = c;
+    }
+    pri += s.priced[c];
+    rep += s.replayed[c];
+    amb += s.ambiguous[c];
+  }
+  se[t] = be, ss[t] = bs, sc[t] = bc, sp[t] = pri, sr[t] = rep, sa[t] = amb;
+  __syncthreads();
+  for (int h = blockDim.x / 2; h > 0; h >>= 1) {
+    if (t < h) {
+      const int u = t + h;
+      if (sc[u] >= 0 && (sc[t] < 0 || se[u] < se[t] || (se[u] == se[t] && ss[u] < ss[t]))) {
+        se[t] = se[u];
+        ss[t] = ss[u];
+        sc[t] = sc[u];
+      }
+      sp[t] += sp[u];
+      sr[t] += sr[u];
+      sa[t] += sa[u];
+    }
+    __syncthreads();
+  }
+  if (t == 0) {
+    out->champion_chain = sc[0];
+    out->best_energy = se[0];
+    out->best_seed = ss[0];
+    out->priced = sp[0];
+    out->replayed = sr[0];
+    out->ambiguous = sa[0];
+  }
+}
+
+extern "C" {
+
+int sip_anneal_epoch(sip_kernel* k, const sip_anneal_cfg* cfg, int64_t seed_base, int32_t chains,
+                     const uint16_t* start, sip_epoch_result* result, uint16_t* champion) {
+  if (!k || !cfg || !result || !champion) return SIP_E_ARG;
+  int rc = run_fused(k, cfg, nullptr, chains, start, false, seed_base);
+  if (rc != SIP_OK) return rc;
+  sip_ctx* ctx = k->ctx;
+  sip_chains& o = *k->ws;
+  if (!k->d_epoch) {
+    sip_epoch_result* p = nullptr;
+    TRY(dalloc(ctx, &p, 1));
+    k->d_epoch = p;
+  }
+  sip_epoch_result* d_res = static_cast<sip_epoch_result*>(k->d_epoch);
+  epoch_reduce_kernel<<<1, 1024, 0, ctx->stream>>>(o.s, d_res);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(result, d_res, sizeof *result, cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) return fail(ctx, SIP_E_CUDA, std::string("anneal epoch: ") + cudaGetErrorString(e));
+  SIP_CUDA(ctx, cudaMemcpyAsync(champion, o.s.best + (size_t)result->champion_chain * o.s.ns,
+                                sizeof(uint16_t) * o.s.n, cudaMemcpyDeviceToHost, ctx->stream));
+  SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return SIP_OK;
 }
 

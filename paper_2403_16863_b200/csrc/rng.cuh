@@ -56,11 +56,28 @@ __host__ __device__ inline void mt_init_by_array(MtRef& m, const uint32_t* base,
     }
     if (j >= klen) j = 0;
   }
-  for (int k = MT_N - 1; k; --k) {
-    uint32_t v = (m.at(i) ^ ((prev ^ (prev >> 30)) * 1566083941u)) - (uint32_t)i;
-    m.at(i) = v;
-    prev = v;
-    ++i;
+  // second pass: eight words per step with their loads issued first (the chain
+  // through `prev` is serial, the words it mixes in are not)
+  for (int k = MT_N - 1; k;) {
+    if (k >= 8 && i + 8 <= MT_N) {
+      uint32_t w[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) w[u] = m.at(i + u);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        uint32_t v = (w[u] ^ ((prev ^ (prev >> 30)) * 1566083941u)) - (uint32_t)(i + u);
+        m.at(i + u) = v;
+        prev = v;
+      }
+      i += 8;
+      k -= 8;
+    } else {
+      uint32_t v = (m.at(i) ^ ((prev ^ (prev >> 30)) * 1566083941u)) - (uint32_t)i;
+      m.at(i) = v;
+      prev = v;
+      ++i;
+      --k;
+    }
     if (i >= MT_N) {
       m.at(0) = m.at(MT_N - 1);
       prev = m.at(0);
@@ -71,18 +88,21 @@ __host__ __device__ inline void mt_init_by_array(MtRef& m, const uint32_t* base,
   m.mti = MT_N;
 }
 
-__host__ __device__ inline void mt_twist(MtRef& m) {
-  for (int i = 0; i < MT_N; ++i) {
+// Lazy twist: word i of a new round is regenerated right before it is tempered.
+// The textbook twist's step i reads slots i, i+1 (both not yet regenerated) and
+// i+397 mod 624 (not yet regenerated for i < 227, already regenerated for
+// i >= 227), so doing step i on demand yields exactly the same words; a chain
+// that draws ~200 numbers no longer regenerates all 624.  mti == 624 after
+// seeding still means "start a new round".
+__host__ __device__ inline uint32_t mt_next(MtRef& m) {
+  if (m.mti >= MT_N) m.mti = 0;
+  {
+    const int i = m.mti;
     uint32_t y = (m.at(i) & 0x80000000u) | (m.at(i + 1 < MT_N ? i + 1 : 0) & 0x7fffffffu);
     int j = i + MT_M;
     if (j >= MT_N) j -= MT_N;
     m.at(i) = m.at(j) ^ (y >> 1) ^ ((y & 1u) ? 0x9908b0dfu : 0u);
   }
-  m.mti = 0;
-}
-
-__host__ __device__ inline uint32_t mt_next(MtRef& m) {
-  if (m.mti >= MT_N) mt_twist(m);
   uint32_t y = m.at(m.mti++);
   y ^= (y >> 11);
   y ^= (y << 7) & 0x9d2c5680u;

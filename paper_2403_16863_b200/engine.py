@@ -62,6 +62,12 @@ SUMMARY_DTYPE = np.dtype([("t0", "<f8"), ("best_energy", "<f8"), ("current_energ
                           ("priced", "<i4"), ("pad", "<i4")])
 
 
+class EpochResult(ctypes.Structure):
+    _fields_ = [("champion_chain", ctypes.c_int32), ("pad", ctypes.c_int32), ("best_energy", ctypes.c_double),
+                ("best_seed", ctypes.c_int64), ("priced", ctypes.c_int64), ("replayed", ctypes.c_int64),
+                ("ambiguous", ctypes.c_int64)]
+
+
 class Launch(ctypes.Structure):
     _fields_ = [("grid", ctypes.c_uint32 * 3), ("block", ctypes.c_uint32 * 3),
                 ("cluster", ctypes.c_uint32 * 3), ("smem_bytes", ctypes.c_uint32),
@@ -98,6 +104,8 @@ _SIGS = {
                     ctypes.c_void_p, c_u16p, c_u16p, ctypes.c_void_p], ctypes.c_int),
     "sip_anneal_ex": ([ctypes.c_void_p, ctypes.POINTER(AnnealCfg), c_i64p, ctypes.c_int32, c_u16p,
                        ctypes.c_void_p, c_u16p, c_u16p, ctypes.c_void_p, c_u16p, c_i32p], ctypes.c_int),
+    "sip_anneal_epoch": ([ctypes.c_void_p, ctypes.POINTER(AnnealCfg), ctypes.c_int64, ctypes.c_int32, c_u16p,
+                          ctypes.c_void_p, c_u16p], ctypes.c_int),
     "sip_anneal_keep": ([ctypes.c_void_p, ctypes.POINTER(AnnealCfg), c_i64p, ctypes.c_int32, c_u16p,
                          ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
     "sip_results_fetch": ([ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, c_u16p, c_u16p],
@@ -344,6 +352,22 @@ class DeviceKernel:
             None if hist is None else hist.ctypes.data_as(ctypes.c_void_p), None, None,
             summ.ctypes.data_as(ctypes.c_void_p), _ptr(champ, c_u16p), ctypes.byref(wch)))
         return hist, summ, champ, wch.value
+
+    def anneal_epoch_reduced(self, seed_base: int, chains: int, temps: np.ndarray, start=None,
+                             unsafe: bool = False):
+        """One sharded-search epoch (sip_anneal_epoch): `chains` fused chains with seeds
+        seed_base + c generated on the device, reduced there to the champion under
+        driver.py:81-85's ranking plus instrumentation sums.  Returns (dict, schedule)."""
+        temps = np.ascontiguousarray(temps, dtype=np.float64)
+        champ = np.zeros(self.n, dtype=np.uint16)
+        st = None if start is None else np.ascontiguousarray(start, dtype=np.uint16)
+        res = EpochResult()
+        cfg = self._cfg(temps, unsafe, False, 0)
+        self.ctx.check(self.ctx.lib.sip_anneal_epoch(
+            self.handle, ctypes.byref(cfg), int(seed_base), int(chains),
+            None if st is None else _ptr(st, c_u16p), ctypes.byref(res), _ptr(champ, c_u16p)))
+        out = {f: getattr(res, f) for f, _ in EpochResult._fields_ if f != "pad"}
+        return out, champ
 
     def anneal_keep(self, seeds, temps: np.ndarray, start=None, unsafe: bool = False,
                     hw_safe: bool = False, min_fixed: int = 0):

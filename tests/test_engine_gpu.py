@@ -150,3 +150,21 @@ def test_anneal_epoch_restart_matches_oracle_from_identity():
         best_e.append((os_["best_energy"], int(s), ob))
     e, s, ob = min(best_e, key=lambda x: (x[0], x[1]))
     assert seeds[w] == s and np.array_equal(champ, ob)
+
+
+def test_anneal_epoch_reduced_matches_oracle_champion():
+    """sip_anneal_epoch: device seeds seed_base + c, champion and sums reduced on the
+    device, equal to the oracle's chains ranked like driver.py:81-85."""
+    rec, k, t, dk = setup("synthetic_mix_2")
+    temps = AnnealConfig().temperatures()
+    res, champ = dk.anneal_epoch_reduced(700, 96, temps)
+    ol = oracle.OracleListing(t)
+    best_e, priced = [], 0
+    for s in range(700, 796):
+        oh, ob, _, os_ = ol.anneal(s, temps)
+        best_e.append((os_["best_energy"], s, ob))
+        priced += int((oh["status"] <= 1).sum())
+    e, s, ob = min(best_e, key=lambda x: (x[0], x[1]))
+    assert res["best_seed"] == s and res["champion_chain"] == s - 700
+    assert res["best_energy"] == e and np.array_equal(champ, ob)
+    assert res["priced"] == priced and res["ambiguous"] == 0

@@ -25,8 +25,9 @@ elif which == "engine":
     L = decoded_listing()
     dk = get_context().kernel(KernelTables.build(L.kernel, MachineConfig()))
     temps = AnnealConfig().temperatures()
+    C = int(sys.argv[2]) if len(sys.argv) > 2 else 32768
     for r in range(2):
-        dk.anneal_epoch(np.arange(32768) + r * 32768, temps, with_history=False)
+        dk.anneal_epoch(np.arange(C) + r * C, temps, with_history=False)
 elif which == "verify":
     from paper_2403_16863_b200.verify import Verifier
     v = Verifier("gemm")
