@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--sim-chains", type=int, default=131072, help="engine chains per GPU")
+    ap.add_argument("--sim-chains", type=int, default=262144, help="engine chains per GPU")
     ap.add_argument("--chains", type=int, default=16, help="hardware-priced chains per GPU")
     ap.add_argument("--hw-steps", type=int, default=24, help="hardware search rounds")
     ap.add_argument("--classes", default="extended", choices=["global", "extended"],

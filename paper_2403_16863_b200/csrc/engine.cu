@@ -373,30 +373,45 @@ __device__ void chain_init(const KernelDev& d, const int16_t* gid, const Chains&
 #endif
 constexpr int CK = SIP_CK;
 
-__device__ __forceinline__ void ck_put(int32_t* base, int C, int c, int j, const Sb& st) {
-  size_t i = (size_t)j * 8 * C + c;
-  base[i] = st.ptr;
-  base[i + C] = st.fin;
-#pragma unroll
-  for (int b = 0; b < 6; ++b) base[i + (size_t)(2 + b) * C] = st.clr[b];
+// checkpoints are chain-major, [C][nck][8] int32: one chain's state at one
+// checkpoint is a single 32-byte sector (two 16-byte accesses).  Lanes of a warp
+// sit at different checkpoints (different lo), so position-major rows gave each
+// field its own sector.
+__device__ __forceinline__ int4* ck_at(int32_t* base, const Chains& s, int c, int j) {
+  return reinterpret_cast<int4*>(base + ((size_t)c * s.nck + j) * 8);
+}
+__device__ __forceinline__ const int4* ck_at(const int32_t* base, const Chains& s, int c, int j) {
+  return reinterpret_cast<const int4*>(base + ((size_t)c * s.nck + j) * 8);
 }
 
-__device__ __forceinline__ void ck_get(const int32_t* base, int C, int c, int j, Sb& st) {
-  size_t i = (size_t)j * 8 * C + c;
-  st.ptr = base[i];
-  st.fin = base[i + C];
-#pragma unroll
-  for (int b = 0; b < 6; ++b) st.clr[b] = base[i + (size_t)(2 + b) * C];
+__device__ __forceinline__ void ck_put(int32_t* base, const Chains& s, int c, int j, const Sb& st) {
+  int4* o = ck_at(base, s, c, j);
+  o[0] = make_int4(st.ptr, st.fin, st.clr[0], st.clr[1]);
+  o[1] = make_int4(st.clr[2], st.clr[3], st.clr[4], st.clr[5]);
 }
 
-__device__ __forceinline__ bool ck_shift(const int32_t* base, int C, int c, int j, const Sb& st, int& delta) {
-  size_t i = (size_t)j * 8 * C + c;
-  const int ptr = base[i];
-  const int dl = st.ptr - ptr;
-  if (max(st.fin, st.ptr) != max(base[i + C], ptr) + dl) return false;
+__device__ __forceinline__ void ck_get(const int32_t* base, const Chains& s, int c, int j, Sb& st) {
+  const int4* o = ck_at(base, s, c, j);
+  const int4 a = o[0], b = o[1];
+  st.ptr = a.x;
+  st.fin = a.y;
+  st.clr[0] = a.z;
+  st.clr[1] = a.w;
+  st.clr[2] = b.x;
+  st.clr[3] = b.y;
+  st.clr[4] = b.z;
+  st.clr[5] = b.w;
+}
+
+__device__ __forceinline__ bool ck_shift(const int32_t* base, const Chains& s, int c, int j, const Sb& st,
+                                         int& delta) {
+  Sb k;
+  ck_get(base, s, c, j, k);
+  const int dl = st.ptr - k.ptr;
+  if (max(st.fin, st.ptr) != max(k.fin, k.ptr) + dl) return false;
 #pragma unroll
   for (int b = 0; b < 6; ++b)
-    if (max(st.clr[b], st.ptr) != max(base[i + (size_t)(2 + b) * C], ptr) + dl) return false;
+    if (max(st.clr[b], st.ptr) != max(k.clr[b], k.ptr) + dl) return false;
   delta = dl;
   return true;
 }
@@ -430,10 +445,10 @@ __device__ int ck_price(const uint2* meta, const Chains& s, int c, int lo, int t
   const int C = s.C, n = s.n;
   int j0 = lo / CK;
   Sb st;
-  ck_get(s.ckpt, C, c, j0, st);
+  ck_get(s.ckpt, s, c, j0, st);
   replay_span(meta, row, j0 * CK, lo, st);
   st.step(meta[row[lo + 1]]);
-  if ((lo + 1) % CK == 0) ck_put(s.ckpt2, C, c, (lo + 1) / CK, st);
+  if ((lo + 1) % CK == 0) ck_put(s.ckpt2, s, c, (lo + 1) / CK, st);
   st.step(meta[row[lo]]);
   int p = lo + 2;
   int pb = min(n, ((p + CK - 1) / CK) * CK);
@@ -442,11 +457,11 @@ __device__ int ck_price(const uint2* meta, const Chains& s, int c, int lo, int t
   delta = 0;
   for (p = pb; p < n; p += CK) {
     int j = p / CK;
-    if (ck_shift(s.ckpt, C, c, j, st, delta)) {
+    if (ck_shift(s.ckpt, s, c, j, st, delta)) {
       jconv = j;
       return total_x + delta;
     }
-    ck_put(s.ckpt2, C, c, j, st);
+    ck_put(s.ckpt2, s, c, j, st);
     int pe = min(n, p + CK);
     replay_span(meta, row, p, pe, st);
     steps += pe - p;
@@ -459,15 +474,17 @@ __device__ int ck_price(const uint2* meta, const Chains& s, int c, int lo, int t
 // jconv, the current ones shifted by delta from jconv on
 __device__ void ck_commit(const Chains& s, int c, int lo, int jconv, int delta) {
   for (int j = (lo + CK) / CK; j < jconv; ++j) {
-    size_t i = (size_t)j * 8 * s.C + c;
-#pragma unroll
-    for (int f = 0; f < 8; ++f) s.ckpt[i + (size_t)f * s.C] = s.ckpt2[i + (size_t)f * s.C];
+    int4* d = ck_at(s.ckpt, s, c, j);
+    const int4* x = ck_at(s.ckpt2, s, c, j);
+    d[0] = x[0];
+    d[1] = x[1];
   }
   if (delta != 0)
     for (int j = jconv; j < s.nck; ++j) {
-      size_t i = (size_t)j * 8 * s.C + c;
-#pragma unroll
-      for (int f = 0; f < 8; ++f) s.ckpt[i + (size_t)f * s.C] += delta;
+      int4* d = ck_at(s.ckpt, s, c, j);
+      int4 a = d[0], b = d[1];
+      d[0] = make_int4(a.x + delta, a.y + delta, a.z + delta, a.w + delta);
+      d[1] = make_int4(b.x + delta, b.y + delta, b.z + delta, b.w + delta);
     }
 }
 
@@ -489,19 +506,9 @@ __global__ void start_ckpt_kernel(KernelDev d, Chains s) {
 }
 
 __device__ int ck_copy_start(const Chains& s, int c) {
-  for (int j = 0; j < s.nck; ++j) {
-    const int4* src = reinterpret_cast<const int4*>(s.ck0 + (size_t)j * 8);
-    const int4 a = src[0], b = src[1];
-    size_t i = (size_t)j * 8 * s.C + c;
-    s.ckpt[i] = a.x;
-    s.ckpt[i + s.C] = a.y;
-    s.ckpt[i + 2 * (size_t)s.C] = a.z;
-    s.ckpt[i + 3 * (size_t)s.C] = a.w;
-    s.ckpt[i + 4 * (size_t)s.C] = b.x;
-    s.ckpt[i + 5 * (size_t)s.C] = b.y;
-    s.ckpt[i + 6 * (size_t)s.C] = b.z;
-    s.ckpt[i + 7 * (size_t)s.C] = b.w;
-  }
+  const int4* src = reinterpret_cast<const int4*>(s.ck0);
+  int4* dst = ck_at(s.ckpt, s, c, 0);
+  for (int q = 0; q < 2 * s.nck; ++q) dst[q] = src[q];
   return s.ck0[(size_t)s.nck * 8];
 }
 
