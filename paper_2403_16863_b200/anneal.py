@@ -219,6 +219,9 @@ def _permuted(kernel: Kernel, perm) -> Kernel:
 _TABLES: dict = {}  # (id(kernel), machine, classes) -> (kernel, tables): listings are reused
 
 
+_DEVICE_KERNELS: dict = {}
+
+
 def device_kernel(kernel: Kernel, machine: MachineConfig | None = None, tables: KernelTables | None = None,
                   classes: str = "global"):
     if tables is None:
@@ -230,7 +233,17 @@ def device_kernel(kernel: Kernel, machine: MachineConfig | None = None, tables: 
             hit = (kernel, KernelTables.build(kernel, machine, classes=classes))
             _TABLES[key] = hit
         tables = hit[1]
-    return get_context().kernel(tables)
+    # one DeviceKernel per table set: its legality rows, baseline and chain workspace
+    # (~10 KB per chain) are reused by later searches instead of rebuilt per call
+    ctx = get_context()
+    dkey = (id(tables), id(ctx))
+    hit = _DEVICE_KERNELS.get(dkey)
+    if hit is None or hit[0] is not tables:
+        if len(_DEVICE_KERNELS) >= 4:
+            _DEVICE_KERNELS.pop(next(iter(_DEVICE_KERNELS)))
+        hit = (tables, ctx.kernel(tables))
+        _DEVICE_KERNELS[dkey] = hit
+    return hit[1]
 
 
 class BatchStates:

@@ -72,4 +72,5 @@ struct sip_kernel {
   struct sip_chains* ws = nullptr;  // reusable chain workspace of sip_anneal_ex
   uint32_t* d_base = nullptr;   // MT19937 init_genrand(19650218) state
   void* d_epoch = nullptr;      // sip_epoch_result of the last sip_anneal_epoch
+  struct sip_chains* spare = nullptr;  // a released result workspace kept for reuse
 };

@@ -981,6 +981,10 @@ int sip_kernel_destroy(sip_kernel* k) {
   }
   if (k->d_base) cudaFree(k->d_base);
   if (k->d_epoch) cudaFree(k->d_epoch);
+  if (k->spare) {
+    chains_free(k->spare);
+    delete k->spare;
+  }
   KernelDev& d = k->d;
   void* ptrs[] = {d.meta, d.klass, d.reads, d.writes, d.refs, d.nrefs, d.cut,
                   d.pin,  d.gid,   d.gids,  d.e_after, d.e_before};
@@ -1090,7 +1094,16 @@ static int run_fused(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* se
     k->ws = nullptr;
   }
   int rc = SIP_OK;
-  if (!k->ws) {
+  if (!k->ws && k->spare && k->spare->s.C == chains && k->spare->s.budget == cfg->budget) {
+    k->ws = k->spare;  // a released result set of the same shape: reuse its buffers
+    k->spare = nullptr;
+    Chains& s = k->ws->s;
+    s.unsafe = cfg->unsafe_moves;
+    s.hw_safe = cfg->hw_safe;
+    s.minfix = cfg->min_fixed_distance;
+    TRY(h2d(ctx, k->ws->d_temps, cfg->temperature, (size_t)s.budget));
+    if (seeds) TRY(h2d(ctx, k->ws->d_seeds, seeds, (size_t)chains));
+  } else if (!k->ws) {
     k->ws = new sip_chains();
     k->ws->k = k;
     rc = chains_alloc(ctx, k, cfg, chains, seeds, k->ws);
@@ -1367,6 +1380,8 @@ int sip_results_destroy(sip_results* r) {
   if (r->ws) {
     if (r->k && !r->k->ws) {
       r->k->ws = r->ws;  // hand the buffers back for the next call
+    } else if (r->k && !r->k->spare) {
+      r->k->spare = r->ws;  // keep one more set of the same shape for the next call
     } else {
       chains_free(r->ws);
       delete r->ws;

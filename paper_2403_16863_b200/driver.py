@@ -19,6 +19,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass, replace
 
+import numpy as np
+
 from .anneal import AnnealConfig, AnnealState, anneal_batch_sim, anneal_steps, uses_device_energy
 from .ir import Kernel
 from .perturb import candidates
@@ -114,9 +116,11 @@ def run_states(kernel: Kernel, backend, cfg: AnnealConfig, chains: int, tester=N
     cfg = hardware_config(backend, cfg)
     if tables is None and hasattr(backend, "tables_for"):
         tables = backend.tables_for(kernel, cfg.candidate_classes)
-    seeds = [cfg.seed + c for c in range(chains)]
     if tester is None and uses_device_energy(backend):
+        # consecutive seeds (driver.py:73-79) as one int64 array: no per-chain Python objects
+        seeds = np.arange(chains, dtype=np.int64) + np.int64(cfg.seed)
         return anneal_batch_sim(kernel, backend.machine, cfg, seeds, tables=tables)
+    seeds = [cfg.seed + c for c in range(chains)]
     if getattr(backend, "batched_chains", False):
         return anneal_steps(kernel, backend, cfg, seeds, tester=tester, tables=tables,
                             on_epoch=on_epoch)
@@ -136,13 +140,12 @@ def run_search(kernel: Kernel, backend, anneal_cfg: AnnealConfig, *, chains: int
                         on_epoch=on_epoch)
     if plan is None and store is None and hasattr(states, "summ"):
         # batched simulator search: rank on the device summaries, build outcomes on access
-        import numpy as np
-
         summ = states.summ
         times = summ["best_energy"] * summ["t0"]
-        seeds = anneal_cfg.seed + np.arange(len(summ))
         lazy = LazyOutcomes(states, anneal_cfg.seed)
-        best = lazy[int(np.lexsort((seeds, times))[0])] if len(summ) else None
+        # (best_time, seed) ranking (driver.py:81-85): seeds increase with the chain
+        # index, so the first minimum is the champion -- O(C) instead of a sort
+        best = lazy[int(np.argmin(times))] if len(summ) else None
         baseline = float(summ["t0"][-1]) if len(summ) else 0.0
         return SearchReport(kernel, digest, baseline, "cycles", lazy, best, len(candidates(kernel)))
     outcomes = []
