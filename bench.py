@@ -279,6 +279,38 @@ def allreduce(dist, vals, op):
     return t.tolist()
 
 
+def library_tflops(kind, tgt, reps: int = 15) -> dict:
+    """Context only: the same operation through the vendor library on the same inputs
+    (torch.matmul -> cuBLAS; scaled_dot_product_attention -> cuDNN/flash), median of
+    `reps` launches with the same 256 MB L2 flush before each."""
+    import torch
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=tgt.inputs[0].device)
+    if kind == "gemm":
+        A, B = tgt.inputs
+        fn = lambda: torch.matmul(A, B.transpose(1, 2))  # noqa: E731
+        name = "torch.matmul (cuBLAS), fp16, no activation"
+    else:
+        import torch.nn.functional as F
+
+        q, k, v = tgt.inputs
+        fn = lambda: F.scaled_dot_product_attention(q, k, v)  # noqa: E731
+        name = "torch scaled_dot_product_attention, fp16, non-causal"
+    for _ in range(3):
+        fn()
+    ts = []
+    for _ in range(reps):
+        flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = statistics.median(ts)
+    return {"tflops": tgt.flops / ms / 1e9, "ms": ms, "what": name}
+
+
 def hardware_phase(kind, listing, local, rank, world, dist, args, rounds, shape=None):
     """Hardware-priced search on one tuning target: rate, roofline, tuned vs nvcc, verification."""
     import numpy as np
@@ -376,7 +408,8 @@ def hardware_phase(kind, listing, local, rank, world, dist, args, rounds, shape=
                  "search_best_energy": res["best_energy"], "accepted_energy": acc_e,
                  "rejected_by_verification": [{"energy": e, "first_failing_sample": v.first_fail_sample,
                                                "max_abs_err": v.max_abs_err} for e, v in rejected],
-                 "paper_speedup": 1.1227 if kind == "gemm" else 1.062}
+                 "paper_speedup": 1.1227 if kind == "gemm" else 1.062,
+                 "library_tflops": library_tflops(kind, tgt)}
     # every rank verifies its share of the samples (batches rank, rank+world, ...) of the
     # same champion; (passed, failed) sum and the first failing sample is the min over ranks
     best = acc_perm
@@ -391,7 +424,7 @@ def hardware_phase(kind, listing, local, rank, world, dist, args, rounds, shape=
                   "seconds": vsec, "samples_per_s": tot[0] / vsec,
                   "compare_gb_per_s": tot[4] / vsec / 1e9, "ranks": world,
                   "sample": ("one independent 256x256x1024 GEMM+LeakyReLU problem" if kind == "gemm"
-                             else "one independent head, S=256 D=128") + ", Philox inputs; baseline "
+                             else "one independent head, S=512 D=128") + ", Philox inputs; baseline "
                             "and champion launched on it, outputs compared (sip_compare)",
                   "tolerance": {"atol": ver.atol, "rtol": ver.rtol}}
     return {"roofline": roofline, "hw": hw, "tuned": tuned, "verify": verify, "launches": h_launch}

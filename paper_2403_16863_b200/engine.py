@@ -206,6 +206,15 @@ class Context:
         self.handle = h
         self.device = device
         self._kernels: dict = {}
+        self._sm_count = None
+
+    @property
+    def sm_count(self) -> int:
+        if self._sm_count is None:
+            import torch
+
+            self._sm_count = int(torch.cuda.get_device_properties(self.device).multi_processor_count)
+        return self._sm_count
 
     def check(self, rc: int) -> None:
         if rc != SIP_OK:

@@ -22,12 +22,26 @@ from .backends import MeasurementFailed
 from .cubin import Module
 from .engine import SIP_E_MEASURE, CmpResult, c_u16p, get_context
 
-# verification shape per target: one sample = one independent problem of this size
+# verification shape per target: one sample = one independent problem of this size.
+# Shapes are chosen so a batch drives every code path of the target: the GEMM's K=1024
+# wraps its 4-stage ring four times per tile and the batch size leaves a partial last
+# wave (so the 128x128 half-tile tail runs too, see gemm_batch); the attention head's
+# S=512 gives four key blocks, wrapping the 2-stage K/V rings and their phases twice.
 VERIFY_SHAPES = {
     "gemm": dict(M=256, N=256, K=1024),
-    "attn": dict(B=1, H=1, S=256, D=128),
+    "attn": dict(B=1, H=1, S=512, D=128),
 }
-DEFAULT_BATCH = {"gemm": 1024, "attn": 512}
+DEFAULT_BATCH = {"gemm": 1024, "attn": 256}
+
+
+def gemm_batch(sms: int, start: int = 1024) -> int:
+    """Largest batch <= start whose 2*L tiles (M=N=256 -> two 128x256 tiles per
+    sample) end in a last wave at most half full, so the kernel's half-tile tail runs."""
+    for L in range(start, 0, -1):
+        tiles = 2 * L
+        if tiles > sms and 0 < tiles % sms <= sms // 2:
+            return L
+    return start
 TOLERANCE = {"fp16": (1e-2, 1e-2)}
 
 
@@ -61,7 +75,7 @@ class Verifier:
 
         self.kind = kind
         self.ctx = get_context(device)
-        self.batch = batch or DEFAULT_BATCH[kind]
+        self.batch = batch or (gemm_batch(self.ctx.sm_count) if kind == "gemm" else DEFAULT_BATCH[kind])
         sh = dict(VERIFY_SHAPES[kind], **(shape or {}))
         if kind == "gemm":
             self.target = make_target("gemm", L=self.batch, seed=seed, device=device, **sh).allocate()
