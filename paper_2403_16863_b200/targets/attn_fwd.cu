@@ -308,7 +308,10 @@ attn_fwd_f16(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CU
       }
       // rescale O_X (rare) before any P of this step is published: PV_X(t-1) must be
       // complete; the first half of PV_X(t) waits for p_full below
-      if (__any_sync(0xffffffffu, grow && t > 0)) {
+      // rescale O_X (rare) before any P of this step is published: PV_X(t-1) must be
+      // complete; the first half of PV_X(t) waits for p_full below
+      const bool rescale = __any_sync(0xffffffffu, grow && t > 0);
+      if (rescale) {
         mbar_wait(&o_done[x], (t - 1) & 1);
         tc_fence_after();
         if (grow && t > 0) {
@@ -344,6 +347,10 @@ attn_fwd_f16(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CU
         tmem_st32(tS(x) + lane_off + hh * (CW / 2) + c * 32, pk);
         // publish this half of P_X(t) (and, with it, any O rescale above)
         tmem_st_wait();
+        // observe o_done's phase t-1 once per step (synccheck: no unobserved phases).
+        // S_X(t) completing implied PV_X(t-1) had, tcgen05.mma running in issue order,
+        // so this returns at once; it must precede the arrive that lets PV_X(t) start.
+        if (c == 0 && t > 0 && !rescale) mbar_wait(&o_done[x], (t - 1) & 1);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[2 * x + hh * (CW / 64) + c]);
