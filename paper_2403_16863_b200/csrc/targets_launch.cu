@@ -95,15 +95,17 @@ int sip_target_attn_launch(sip_ctx* ctx, const void* Q, const void* K, const voi
   std::memcpy(p + 404, &D, 4);
   std::memcpy(p + 408, &scale, 4);
   std::memset(launch, 0, sizeof *launch);
-  launch->grid[0] = (uint32_t)(S / 256);  // two 128-row query tiles per CTA
-  launch->grid[1] = (uint32_t)(B * H);
+  // persistent: one CTA per SM walks the (query-tile pair, head) items
+  long items = (long)(S / 256) * B * H;
+  launch->grid[0] = (uint32_t)(items < ctx->sm_count ? items : ctx->sm_count);
+  launch->grid[1] = 1;
   launch->grid[2] = 1;
-  launch->block[0] = 384;  // warpgroup 0 (TMA, MMA) + one softmax warpgroup per tile (SIP_SPLIT 1)
+  launch->block[0] = 512;  // TMA + MMA warps, 2 softmax warpgroups, 1 epilogue warpgroup
   launch->block[1] = launch->block[2] = 1;
   launch->cluster[0] = launch->cluster[1] = launch->cluster[2] = 1;
-  // Q 2 tiles, K and V 2 stages each; 1 KB alignment slack; 144 B of mbarriers (+ the
-  // TMEM slot); 4 KB of row max / sum exchange (used when the softmax splits a row)
-  launch->smem_bytes = 6 * 128 * 128 * 2 + 1024 + 144 + 4096;
+  // Q 2 tiles, K and V 2 stages each; 1 KB alignment slack; 256 B of mbarriers (+ the
+  // TMEM slot); 1 KB of row sums handed from the softmax to the epilogue warps
+  launch->smem_bytes = 6 * 128 * 128 * 2 + 1024 + 256 + 1024;
   launch->params = params;
   launch->param_offsets = kAttnOffsets;
   launch->nparams = 9;

@@ -13,14 +13,17 @@ for a in sys.argv[1:]:
     variants[path.split("/")[-1]] = path
     if nt:
         threads[path.split("/")[-1]] = int(nt)
-tgt = AttnTarget(B=4, H=32, S=4096).allocate()
+import os
+tgt = AttnTarget(B=int(os.environ.get("AB_B", 4)), H=32, S=int(os.environ.get("AB_S", 4096))).allocate()
 ctx = get_context()
 mods = {k: Module(open(v, 'rb').read(), "attn_fwd_f16", ctx=ctx) for k, v in variants.items()}
 for rnd in range(3):
     for k, m in mods.items():
         lp, params = tgt.launch()
-        if k in threads:
+        if k in threads:  # the non-persistent layout: (S/256, B*H) grid of 384-thread CTAs
             lp.block[0] = threads[k]
+            lp.grid[0], lp.grid[1] = tgt.S // 256, tgt.B * tgt.H
+            lp.smem_bytes = 6 * 128 * 128 * 2 + 1024 + 144 + 4096
         med = ctypes.c_double(); raw = np.zeros(10)
         ctx.check(ctx.lib.sip_measure(m.handle, None, ctypes.byref(lp), 2, 10, 0, ctypes.byref(med),
                                       raw.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
