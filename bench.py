@@ -279,6 +279,21 @@ def allreduce(dist, vals, op):
     return t.tolist()
 
 
+def time_flush(device: int, reps: int = 10) -> float:
+    """Device time (ms) of the evaluator's L2 flush: a 256 MB memset."""
+    import torch
+
+    buf = torch.empty(256 << 20, dtype=torch.uint8, device=torch.device("cuda", device))
+    buf.fill_(0)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for r in range(reps):
+        buf.fill_(r & 0xFF)
+    e1.record()
+    e1.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
 def library_tflops(kind, tgt, reps: int = 15) -> dict:
     """Context only: the same operation through the vendor library on the same inputs
     (torch.matmul -> cuBLAS; scaled_dot_product_attention -> cuDNN/flash), median of
@@ -372,15 +387,21 @@ def hardware_phase(kind, listing, local, rank, world, dist, args, rounds, shape=
                                 "the timed region)" if sustained else
                                 "MEASURED_PEAKS.json bf16_tflops (burst)") if pk["src"] == "measured"
                 else "fallback 1590 TFLOP/s"}
-    floor_ms = (2 if be.paired else 1) * (be.warmup + hcfg.measure_reps) * avg_ms
+    # the evaluator's device work per candidate: (warmup + reps) launches of each schedule
+    # of the pair, plus the 256 MB L2 flush before every timed launch
+    flush_ms = time_flush(local)
+    npair = 2 if be.paired else 1
+    floor_ms = npair * (be.warmup + hcfg.measure_reps) * avg_ms + npair * hcfg.measure_reps * flush_ms
     hw = {"candidates_per_s": h_eval / (h_ms / 1e3), "rounds": rounds, "chains_per_gpu": args.chains,
           "candidate_classes": args.classes, "candidates_in_listing": int(hs.dk.k),
           "proposals": rounds * args.chains * world, "priced": int(h_eval),
           "evaluator_roofline_candidates_per_s": world * 1e3 / floor_ms,
           "device_busy_frac": (h_eval / (h_ms / 1e3)) / (world * 1e3 / floor_ms),
-          "note": "one candidate = re-encode + cuModuleLoadData + one CUDA graph of 2 warmup + 5 timed "
-                  "(nvcc, candidate) launch pairs, L2 flushed before each launch; energy = median "
-                  "pair ratio; roofline = 14 x kernel time"}
+          "flush_ms": flush_ms,
+          "note": "one candidate = re-encode + cuModuleLoadData (8 host threads) + 2 warmup + 5 timed "
+                  "(nvcc, candidate) launch pairs, L2 flushed before each timed launch; a round's "
+                  "candidates share one CUDA graph; energy = median pair ratio; roofline = device "
+                  "time of those 14 launches + 10 flushes"}
     res = hs.result()
     if dist:
         hs.exchange()

@@ -216,6 +216,13 @@ int sip_measure_paired(sip_module* m, const uint16_t* perm_ref, const uint16_t* 
                        const sip_launch* launch, int32_t warmup, int32_t reps, int32_t flush_l2,
                        double* ratio_median, double* ref_median_ms, double* cand_median_ms,
                        double* raw_ratio);
+/* k candidates (perms: [k][n]) each timed against perm_ref like sip_measure_paired,
+ * all from one CUDA graph after parallel cubin loads; per-candidate outputs, and
+ * status[i] = SIP_E_MEASURE for a candidate whose cubin failed to load (skipped). */
+int sip_measure_paired_batch(sip_module* m, const uint16_t* perm_ref, const uint16_t* perms, int32_t k,
+                             const sip_launch* launch, int32_t warmup, int32_t reps, int32_t flush_l2,
+                             double* ratio_median, double* ref_median_ms, double* cand_median_ms,
+                             double* raw_ratio, int32_t* status);
 /* run the permuted module once on the given launch (verification) */
 int sip_run(sip_module* m, const uint16_t* perm, const sip_launch* launch);
 /* same, enqueued on the context stream without synchronising (errors surface at

@@ -18,6 +18,7 @@
 #include <cstring>
 #include <list>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.h"
@@ -118,6 +119,7 @@ struct sip_module {
   std::vector<uint8_t> pin;
   std::vector<uint8_t> patched;
   std::list<CachedMod> cache;  // stable addresses: callers hold CachedMod* across loads
+  size_t cache_cap = 4;        // modules kept loaded (raised for a batch)
   uint64_t clock = 0;
   std::vector<cudaEvent_t> events;
 };
@@ -192,7 +194,7 @@ int get_module(sip_module* m, const uint16_t* perm, CachedMod** out) {
     return cu_fail(ctx, SIP_E_MEASURE, "cuModuleGetFunction", r);
   }
   cm.stamp = ++m->clock;
-  if (m->cache.size() >= 4) {
+  if (m->cache.size() >= m->cache_cap) {
     auto victim = std::min_element(m->cache.begin(), m->cache.end(),
                                    [](const CachedMod& a, const CachedMod& b) { return a.stamp < b.stamp; });
     ctx->cuModuleUnload(victim->mod);
@@ -475,6 +477,133 @@ int sip_measure_paired(sip_module* m, const uint16_t* perm_ref, const uint16_t* 
   *ratio_median = median_of(ratio);
   if (ref_median_ms) *ref_median_ms = median_of(t[0]);
   if (cand_median_ms) *cand_median_ms = median_of(t[1]);
+  return SIP_OK;
+}
+
+// Batched paired timing (the hardware search prices one candidate per live chain per
+// round): the candidates' cubins are patched and loaded on a few host threads, then
+// every candidate's (warmup + reps) interleaved pairs with the baseline run from ONE
+// CUDA graph, so the GPU does not idle between candidates for loads, graph builds and
+// host round trips.  status[i] = SIP_OK or SIP_E_MEASURE (that candidate is skipped).
+int sip_measure_paired_batch(sip_module* m, const uint16_t* perm_ref, const uint16_t* perms, int32_t k,
+                             const sip_launch* L, int32_t warmup, int32_t reps, int32_t flush_l2,
+                             double* ratio_median, double* ref_median_ms, double* cand_median_ms,
+                             double* raw_ratio, int32_t* status) {
+  if (!m || !L || !m->ctx || !perms || k < 1 || !ratio_median || !status || reps < 1 || warmup < 0)
+    return SIP_E_ARG;
+  sip_ctx* ctx = m->ctx;
+  if (m->cache_cap < (size_t)k + 1) m->cache_cap = (size_t)k + 1;
+  CachedMod* ref = nullptr;
+  int rc = get_module(m, perm_ref, &ref);
+  if (rc != SIP_OK) return rc;
+  ref->stamp = ~0ull >> 1;  // the baseline is reused by every batch: never the eviction victim
+  // images + parallel cuModuleLoadData for the candidates not loaded yet
+  std::vector<CachedMod*> mods(k, nullptr);
+  std::vector<int> todo;
+  for (int i = 0; i < k; ++i) {
+    const uint16_t* p = perms + (size_t)i * m->n;
+    std::vector<uint16_t> key(p, p + m->n);
+    for (auto& c : m->cache)
+      if (c.perm == key) {
+        c.stamp = ++m->clock;
+        mods[i] = &c;
+      }
+    status[i] = SIP_OK;
+    if (!mods[i]) todo.push_back(i);
+  }
+  std::vector<std::vector<uint8_t>> imgs(todo.size());
+  std::vector<CUmodule> loaded(todo.size(), nullptr);
+  std::vector<CUresult> lres(todo.size(), CUDA_SUCCESS);
+  for (size_t t = 0; t < todo.size(); ++t)
+    if (build_image(m, perms + (size_t)todo[t] * m->n, imgs[t]) != SIP_OK) lres[t] = CUDA_ERROR_INVALID_IMAGE;
+  const int nthreads = (int)std::min<size_t>(todo.size(), 8);
+  std::vector<std::thread> pool;
+  for (int w = 0; w < nthreads; ++w)
+    pool.emplace_back([&, w]() {
+      cudaSetDevice(ctx->device);  // make the primary context current in this thread
+      for (size_t t = w; t < todo.size(); t += nthreads)
+        if (lres[t] == CUDA_SUCCESS) lres[t] = ctx->cuModuleLoadData(&loaded[t], imgs[t].data());
+    });
+  for (auto& th : pool) th.join();
+  for (size_t t = 0; t < todo.size(); ++t) {
+    const int i = todo[t];
+    if (lres[t] != CUDA_SUCCESS) {
+      status[i] = SIP_E_MEASURE;
+      continue;
+    }
+    CachedMod cm;
+    cm.perm.assign(perms + (size_t)i * m->n, perms + (size_t)(i + 1) * m->n);
+    cm.mod = loaded[t];
+    if (ctx->cuModuleGetFunction(&cm.fn, cm.mod, m->func.c_str()) != CUDA_SUCCESS) {
+      ctx->cuModuleUnload(cm.mod);
+      status[i] = SIP_E_MEASURE;
+      continue;
+    }
+    cm.stamp = ++m->clock;
+    while (m->cache.size() >= m->cache_cap) {  // evict the oldest, never this batch's
+      auto victim = std::min_element(m->cache.begin(), m->cache.end(),
+                                     [](const CachedMod& a, const CachedMod& b) { return a.stamp < b.stamp; });
+      ctx->cuModuleUnload(victim->mod);
+      m->cache.erase(victim);
+    }
+    m->cache.push_back(cm);
+    mods[i] = &m->cache.back();
+  }
+  if (flush_l2 && (rc = ensure_flush(ctx)) != SIP_OK) return rc;
+  const int nev = 4 * reps * k;
+  while ((int)m->events.size() < nev) {
+    cudaEvent_t e;
+    SIP_CUDA(ctx, cudaEventCreate(&e));
+    m->events.push_back(e);
+  }
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  SIP_CUDA(ctx, cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  for (int i = 0; i < k && rc == SIP_OK; ++i) {
+    if (status[i] != SIP_OK) continue;
+    CachedMod* pair[2] = {ref, mods[i]};
+    for (int w = 0; w < warmup && rc == SIP_OK; ++w)
+      for (int q = 0; q < 2 && rc == SIP_OK; ++q) rc = launch(m, pair[q], L);
+    for (int r = 0; r < reps && rc == SIP_OK; ++r)
+      for (int q = 0; q < 2 && rc == SIP_OK; ++q) {
+        const int j = (q + r) % 2;  // rotate the order every rep
+        const int e = 4 * (i * reps + r) + 2 * j;
+        if (flush_l2) cudaMemsetAsync(ctx->flush_buf, (r * 2 + q) & 0xff, ctx->flush_bytes, ctx->stream);
+        cudaEventRecordWithFlags(m->events[e], ctx->stream, cudaEventRecordExternal);
+        rc = launch(m, pair[j], L);
+        cudaEventRecordWithFlags(m->events[e + 1], ctx->stream, cudaEventRecordExternal);
+      }
+  }
+  cudaError_t ce = cudaStreamEndCapture(ctx->stream, &graph);
+  if (rc != SIP_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  if (ce != cudaSuccess) return sip::fail(ctx, SIP_E_MEASURE, std::string("capture: ") + cudaGetErrorString(ce));
+  ce = cudaGraphInstantiate(&exec, graph, 0);
+  if (ce == cudaSuccess) ce = cudaGraphLaunch(exec, ctx->stream);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(ctx->stream);
+  for (int i = 0; i < k && ce == cudaSuccess; ++i) {
+    if (status[i] != SIP_OK) continue;
+    std::vector<double> tr(reps), tc(reps), ratio(reps);
+    for (int r = 0; r < reps && ce == cudaSuccess; ++r) {
+      float a = 0.f, b = 0.f;
+      const int e = 4 * (i * reps + r);
+      ce = cudaEventElapsedTime(&a, m->events[e], m->events[e + 1]);
+      if (ce == cudaSuccess) ce = cudaEventElapsedTime(&b, m->events[e + 2], m->events[e + 3]);
+      tr[r] = a;
+      tc[r] = b;
+      ratio[r] = b / a;
+    }
+    ratio_median[i] = median_of(ratio);
+    if (ref_median_ms) ref_median_ms[i] = median_of(tr);
+    if (cand_median_ms) cand_median_ms[i] = median_of(tc);
+    if (raw_ratio) std::copy(ratio.begin(), ratio.end(), raw_ratio + (size_t)i * reps);
+  }
+  if (exec) cudaGraphExecDestroy(exec);
+  cudaGraphDestroy(graph);
+  if (ce != cudaSuccess)
+    return sip::fail(ctx, SIP_E_MEASURE, std::string("timed launches: ") + cudaGetErrorString(ce));
   return SIP_OK;
 }
 

@@ -129,6 +129,9 @@ _SIGS = {
                      ctypes.c_int32, c_dblp, c_dblp], ctypes.c_int),
     "sip_measure_paired": ([ctypes.c_void_p, c_u16p, c_u16p, ctypes.POINTER(Launch), ctypes.c_int32,
                             ctypes.c_int32, ctypes.c_int32, c_dblp, c_dblp, c_dblp, c_dblp], ctypes.c_int),
+    "sip_measure_paired_batch": ([ctypes.c_void_p, c_u16p, c_u16p, ctypes.c_int32, ctypes.POINTER(Launch),
+                                  ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, c_dblp, c_dblp, c_dblp,
+                                  c_dblp, c_i32p], ctypes.c_int),
     "sip_run": ([ctypes.c_void_p, c_u16p, ctypes.POINTER(Launch)], ctypes.c_int),
     "sip_run_async": ([ctypes.c_void_p, c_u16p, ctypes.POINTER(Launch)], ctypes.c_int),
     "sip_verify_open": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p)],

@@ -17,7 +17,7 @@ import numpy as np
 
 from .backends import BackendDescriptor, CostSample, MeasurementFailed
 from .cubin import Listing, Module, render_listing, schedule_perm
-from .engine import SIP_E_MEASURE, EngineError, c_dblp, c_u16p, get_context
+from .engine import SIP_E_MEASURE, EngineError, c_dblp, c_i32p, c_u16p, get_context
 from .ir import Kernel
 from .targets import make_target
 
@@ -107,6 +107,46 @@ class B200Backend:
         self.ctx.check(rc)
         self.kernel_ms.extend([ref_med.value] * reps + [cand_med.value] * reps)
         return r_med.value, raw.tolist()
+
+    def measure_batch(self, perms, reps: int = 5) -> list:
+        """Paired timing of many candidates in one CUDA graph (sip_measure_paired_batch).
+        Returns one CostSample per candidate, or a MeasurementFailed instance for a
+        candidate whose cubin could not be loaded."""
+        perms = np.ascontiguousarray(np.asarray(perms, dtype=np.uint16).reshape(-1, self.listing.n))
+        k = perms.shape[0]
+        if k == 0:
+            return []
+        if not self.paired:
+            return [self._try(lambda p=p: self._measure_single(p, reps)) for p in perms]
+        ratio, refm, candm = (np.zeros(k, dtype=np.float64) for _ in range(3))
+        raw = np.zeros((k, reps), dtype=np.float64)
+        status = np.zeros(k, dtype=np.int32)
+        lib = self.ctx.lib
+        rc = lib.sip_measure_paired_batch(
+            self.module.handle, self.identity.ctypes.data_as(c_u16p), perms.ctypes.data_as(c_u16p), k,
+            ctypes.byref(self.launch), self.warmup, reps, int(self.flush_l2), ratio.ctypes.data_as(c_dblp),
+            refm.ctypes.data_as(c_dblp), candm.ctypes.data_as(c_dblp), raw.ctypes.data_as(c_dblp),
+            status.ctypes.data_as(c_i32p))
+        self.calls += k
+        if rc == SIP_E_MEASURE:
+            raise MeasurementFailed(lib.sip_last_error(self.ctx.handle).decode(errors="replace"))
+        self.ctx.check(rc)
+        out = []
+        for i in range(k):
+            if status[i] != 0:
+                out.append(MeasurementFailed(f"candidate {i}: cubin could not be loaded"))
+                continue
+            self.kernel_ms.extend([float(refm[i])] * reps + [float(candm[i])] * reps)
+            out.append(CostSample(float(ratio[i]) * self.ref_ms, self.unit, reps,
+                                  tuple(float(r) * self.ref_ms for r in raw[i])))
+        return out
+
+    @staticmethod
+    def _try(fn):
+        try:
+            return fn()
+        except MeasurementFailed as exc:
+            return exc
 
     def _measure_single(self, perm, reps: int = 5) -> CostSample:
         perm = np.ascontiguousarray(perm, dtype=np.uint16)

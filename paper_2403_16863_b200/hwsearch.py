@@ -59,14 +59,19 @@ class HardwareSearch:
         self.launches += 1
         live = np.nonzero(lo >= 0)[0]
         n = 0
-        for c in live:
-            try:
-                self.times[c] = self.be.measure_perm(cand[c], self.cfg.measure_reps).value
-                self.status[c] = ST_PRICED
-                n += 1
-                self.launches += self.be.warmup + self.cfg.measure_reps
-            except MeasurementFailed:
+        if len(live) and hasattr(self.be, "measure_batch"):
+            # every live chain's candidate timed in one CUDA graph (parallel cubin loads)
+            samples = self.be.measure_batch(cand[live], self.cfg.measure_reps)
+        else:
+            samples = [self._measure(cand[c]) for c in live]
+        for c, smp in zip(live, samples):
+            if isinstance(smp, MeasurementFailed):
                 self.times[c], self.status[c] = 0.0, ST_MEASURE
+                continue
+            self.times[c] = smp.value
+            self.status[c] = ST_PRICED
+            n += 1
+            self.launches += 2 * (self.be.warmup + self.cfg.measure_reps)
         if len(live):
             self.chains.resolve(self.times, self.status)
             self.launches += 1
@@ -75,6 +80,12 @@ class HardwareSearch:
         if self.epoch and self.rounds % self.epoch == 0:
             self.exchange()
         return n
+
+    def _measure(self, perm):
+        try:
+            return self.be.measure_perm(perm, self.cfg.measure_reps)
+        except MeasurementFailed as exc:
+            return exc
 
     def local_best(self):
         hist, best, cur, summ = self.chains.result()

@@ -188,3 +188,18 @@ def test_every_hw_safe_single_swap_verifies(kind):
         perm[lo], perm[lo + 1] = perm[lo + 1], perm[lo]
         vr = ver.run(perm, 64, fail_fast=True, check_every=1)
         assert vr.ok and vr.bitdiff_elems == 0, (int(lo), str(seq[lo].source_text), str(seq[lo + 1].source_text))
+
+
+def test_measure_batch_paired():
+    """sip_measure_paired_batch: several candidates timed against the nvcc schedule in
+    one graph; identical schedules time as ratio ~1, a bad cubin is reported per
+    candidate instead of failing the batch."""
+    tgt = GemmTarget(M=512, N=512, K=1024).allocate()
+    be = B200Backend(tgt)
+    ident = schedule_perm(be.kernel)
+    perms = np.stack([ident, ident, ident])
+    out = be.measure_batch(perms, reps=5)
+    assert len(out) == 3
+    for smp in out:
+        assert smp.unit == "ms" and len(smp.raw) == 5
+        assert 0.8 * be.ref_ms < smp.value < 1.25 * be.ref_ms
