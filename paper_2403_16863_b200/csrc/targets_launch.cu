@@ -32,8 +32,8 @@ int sip_target_gemm_launch(sip_ctx* ctx, const void* A, const void* B, void* C, 
                            int32_t K, int32_t L, float slope, sip_launch* launch, void* params,
                            uint32_t params_cap) {
   if (!ctx || !A || !B || !C || !launch || !params || params_cap < kGemmParamBytes) return SIP_E_ARG;
-  if (M <= 0 || N <= 0 || K <= 0 || L <= 0 || M % 128 || N % 256 || K % 64)
-    return sip::fail(ctx, SIP_E_ARG, "gemm target needs M%128==0, N%256==0, K%64==0");
+  if (M <= 0 || N <= 0 || K <= 0 || L <= 0 || M % 256 || N % 256 || K % 64)
+    return sip::fail(ctx, SIP_E_ARG, "gemm target needs M%256==0, N%256==0, K%64==0");
   uint8_t* p = static_cast<uint8_t*>(params);
   std::memset(p, 0, kGemmParamBytes);
   cuuint64_t da[3] = {(cuuint64_t)K, (cuuint64_t)M, (cuuint64_t)L};
@@ -41,8 +41,10 @@ int sip_target_gemm_launch(sip_ctx* ctx, const void* A, const void* B, void* C, 
   cuuint32_t ba[3] = {64, 128, 1};
   cuuint64_t db[3] = {(cuuint64_t)K, (cuuint64_t)N, (cuuint64_t)L};
   cuuint64_t sb[2] = {(cuuint64_t)K * 2, (cuuint64_t)N * K * 2};
-  cuuint32_t bb[3] = {64, 256, 1};
-  cuuint32_t bh[3] = {64, 128, 1};  // half-width B box for the 128x128 tail tiles
+  // each CTA of a cluster loads half of the pair's B tile: 128-row boxes for 256-column
+  // tiles, 64-row boxes for the 128-column tail halves
+  cuuint32_t bb[3] = {64, 128, 1};
+  cuuint32_t bh[3] = {64, 64, 1};
   int rc = encode(ctx, reinterpret_cast<CUtensorMap*>(p), A, 3, da, sa, ba);
   if (rc == SIP_OK) rc = encode(ctx, reinterpret_cast<CUtensorMap*>(p + 128), B, 3, db, sb, bb);
   if (rc == SIP_OK) rc = encode(ctx, reinterpret_cast<CUtensorMap*>(p + 256), B, 3, db, sb, bh);
@@ -53,17 +55,18 @@ int sip_target_gemm_launch(sip_ctx* ctx, const void* A, const void* B, void* C, 
   std::memcpy(p + 400, &K, 4);
   std::memcpy(p + 404, &L, 4);
   std::memcpy(p + 408, &slope, 4);
-  // persistent grid: one CTA per SM; problems with at most half as many tiles as SMs
-  // run every tile as two 128x128 halves (see the kernel's Schedule)
-  long tiles = (long)(M / 128) * (N / 256) * L;
-  long sms = ctx->sm_count;
-  long grid = tiles >= sms ? sms : (2 * tiles <= sms ? 2 * tiles : tiles);
+  // persistent clusters of 2 CTAs (tile pairs sharing B), one CTA per SM; problems with at
+  // most half as many pairs as clusters run every pair as two halves (the kernel's Schedule)
+  long pairs = (long)(M / 256) * (N / 256) * L;
+  long cmax = ctx->sm_count / 2;
+  long ncl = pairs >= cmax ? cmax : (2 * pairs <= cmax ? 2 * pairs : pairs);
   std::memset(launch, 0, sizeof *launch);
-  launch->grid[0] = (uint32_t)grid;
+  launch->grid[0] = (uint32_t)(2 * ncl);
   launch->grid[1] = launch->grid[2] = 1;
   launch->block[0] = 192;
   launch->block[1] = launch->block[2] = 1;
-  launch->cluster[0] = launch->cluster[1] = launch->cluster[2] = 1;
+  launch->cluster[0] = 2;  // CTA pairs (the kernel reads %cluster_ctarank)
+  launch->cluster[1] = launch->cluster[2] = 1;
   launch->smem_bytes = 4 * (128 * 64 * 2 + 256 * 64 * 2) + 1024 + 256;
   launch->params = params;
   launch->param_offsets = kGemmOffsets;

@@ -2,14 +2,19 @@
 //
 // The paper's GEMM+LeakyReLU workload, written by hand for
 // sm_100a instead of Triton/A100:
-//   * persistent: one CTA per SM, static round-robin over 128x256 output tiles
-//     (batched over L independent problems, used by the verifier);
-//   * wave-quantisation tail: when the last round of tiles would leave more than
-//     half the SMs idle (4096^3: 512 tiles on 148 SMs, last wave 46 % full), those
-//     tiles are split into two 128x128 halves (N=128 MMA, half-height B box), so
-//     the tail costs half a tile instead of a full one.  Small problems with fewer
-//     than half as many tiles as SMs run as half tiles throughout;
-//   * warp 0: TMA producer (SWIZZLE_128B, 4-stage 48 KB ring, mbarrier full/empty);
+//   * persistent clusters of 2 CTAs (one per SM): the pair computes two M-adjacent
+//     128x256 tiles sharing one 256-row B tile; each CTA loads its own A tile and
+//     HALF of B, multicast into both CTAs' shared memory, so a CTA pulls 32 KB per
+//     k-block from L2 instead of 48 KB (the 1-CTA kernel was bound by L2->SM
+//     traffic: its TMA stream alone took 82 of its 102 us at 4096^3);
+//   * static round-robin over tile pairs (batched over L independent problems,
+//     used by the verifier); wave-quantisation tail: when the last round of pairs
+//     would leave more than half the clusters idle (4096^3: 256 pairs on 74
+//     clusters, last wave 46 % full), those pairs run as two 128-column halves
+//     (N=128 MMA, half-height B boxes), so the tail costs half a pair instead of a
+//     full one; problems with at most half as many pairs as clusters run as halves;
+//   * warp 0: TMA producer (SWIZZLE_128B, 4-stage ring: A 16 KB + B 32 KB, of which
+//     this CTA loads 16 KB and the peer the other 16; "empty" needs both CTAs' MMAs);
 //   * warp 1: TMEM allocator + single-thread tcgen05.mma issuer (M128 N256 K16),
 //     accumulating in one of two 256-column TMEM buffers;
 //   * warps 2-5: epilogue -- tcgen05.ld 32 columns at a time, LeakyReLU in fp32,
@@ -18,7 +23,7 @@
 // The epilogue's STG instructions are the global-memory instructions SIP may move
 // under the reference's candidate rules.
 //
-// Requirements (checked by the host launcher): M % 128 == 0, N % 256 == 0,
+// Requirements (checked by the host launcher): M % 256 == 0, N % 256 == 0,
 // K % 64 == 0; A is [L][M][K], B is [L][N][K], C is [L][M][N], all row-major.
 #include "sm100.cuh"
 
@@ -30,29 +35,29 @@ constexpr int NUM_THREADS = 192;
 constexpr uint32_t IDESC = sm100::idesc_f16(BM, BN);
 constexpr uint32_t IDESC_HALF = sm100::idesc_f16(BM, BN / 2);
 
-// Work item t of the static schedule -> (problem l, m0, n0, half?).
+// Work item t of the cluster's static schedule -> (problem l, m0 of this CTA, n0, half?).
 struct Schedule {
-  int tiles_m, tiles_n, full, items;
-  __device__ Schedule(int M, int N, int L, int grid) {
-    tiles_m = M / BM;
+  int pairs_m, tiles_n, full, items;
+  __device__ Schedule(int M, int N, int L, int nclusters) {
+    pairs_m = M / (2 * BM);
     tiles_n = N / BN;
-    const int tiles = tiles_m * tiles_n * L;
-    const int rem = tiles % grid;
-    if (2 * tiles <= grid) {
-      full = 0;  // few tiles: every tile as two halves
-    } else if (tiles > grid && rem != 0 && 2 * rem <= grid) {
-      full = tiles - rem;  // whole waves of full tiles, tail as halves
+    const int pairs = pairs_m * tiles_n * L;
+    const int rem = pairs % nclusters;
+    if (2 * pairs <= nclusters) {
+      full = 0;  // few pairs: every pair as two halves
+    } else if (pairs > nclusters && rem != 0 && 2 * rem <= nclusters) {
+      full = pairs - rem;  // whole waves of full pairs, tail as halves
     } else {
-      full = tiles;
+      full = pairs;
     }
-    items = full + 2 * (tiles - full);
+    items = full + 2 * (pairs - full);
   }
   __device__ bool half(int t) const { return t >= full; }
-  __device__ void coords(int t, int& l, int& m0, int& n0) const {
-    const int tile = t < full ? t : full + ((t - full) >> 1);
-    l = tile / (tiles_m * tiles_n);
-    const int r = tile % (tiles_m * tiles_n);
-    m0 = (r / tiles_n) * BM;
+  __device__ void coords(int t, int rank, int& l, int& m0, int& n0) const {
+    const int pair = t < full ? t : full + ((t - full) >> 1);
+    l = pair / (pairs_m * tiles_n);
+    const int r = pair % (pairs_m * tiles_n);
+    m0 = ((r / tiles_n) * 2 + rank) * BM;
     n0 = (r % tiles_n) * BN + (t < full ? 0 : ((t - full) & 1) * (BN / 2));
   }
 };
@@ -75,7 +80,9 @@ gemm_lrelu_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   const int warp = warp_id();
   const int lane = threadIdx.x & 31;
   const int kblocks = K / BK;
-  const Schedule sched(M, N, L, gridDim.x);
+  const int rank = (int)cluster_rank();
+  const int cid = (int)cluster_id_x(), ncl = (int)cluster_count_x();
+  const Schedule sched(M, N, L, ncl);
   const int items = sched.items;
 
   if (warp == 0 && elect_one()) {
@@ -84,7 +91,7 @@ gemm_lrelu_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     tma_prefetch(&tmBh);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], 2);  // both CTAs' MMAs: each stage's B holds both CTAs' halves
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
@@ -95,6 +102,7 @@ gemm_lrelu_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   if (warp == 1) tmem_alloc<TMEM_COLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
+  cluster_sync();  // the peer's barriers are initialised before any multicast lands in them
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -103,16 +111,19 @@ gemm_lrelu_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < items; t += gridDim.x) {
+      for (int t = cid; t < items; t += ncl) {
         int l, m0, n0;
-        sched.coords(t, l, m0, n0);
+        sched.coords(t, rank, l, m0, n0);
         const bool half = sched.half(t);
-        const CUtensorMap* mb = half ? &tmBh : &tmB;
+        const int nb = half ? BN / 2 : BN;        // B rows of the tile
+        const CUtensorMap* mb = half ? &tmBh : &tmB;  // boxes of nb / 2 rows
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], half ? A_BYTES + B_BYTES / 2 : STAGE_BYTES);
+          mbar_expect_tx(&full[stage], A_BYTES + nb * BK * 2);
           tma_load_3d(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, m0, l);
-          tma_load_3d(sB + stage * B_BYTES, mb, &full[stage], kb * BK, n0, l);
+          // this CTA's half of B, into the same stage of both CTAs
+          tma_load_3d_mc(sB + stage * B_BYTES + rank * (nb / 2) * BK * 2, mb, &full[stage], kb * BK,
+                         n0 + rank * (nb / 2), l, (uint16_t)0x3);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -125,7 +136,7 @@ gemm_lrelu_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     int stage = 0;
     uint32_t phase = 0;
     int local = 0;
-    for (int t = blockIdx.x; t < items; t += gridDim.x, ++local) {
+    for (int t = cid; t < items; t += ncl, ++local) {
       const int buf = local & 1;
       const uint32_t use = local >> 1;
       const uint32_t idesc = sched.half(t) ? IDESC_HALF : IDESC;
@@ -140,7 +151,7 @@ gemm_lrelu_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk)
             mma_f16(d_tmem, desc_sw128(a0 + kk * 32), desc_sw128(b0 + kk * 32), idesc, (kb | kk) != 0);
-          mma_commit(&empty[stage]);
+          mma_commit_mc(&empty[stage], (uint16_t)0x3);  // frees the stage in both CTAs
           if (kb == kblocks - 1) mma_commit(&acc_full[buf]);
         }
         __syncwarp();
@@ -155,11 +166,11 @@ gemm_lrelu_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int row_in_tile = quarter * 32 + lane;
     int local = 0;
-    for (int t = blockIdx.x; t < items; t += gridDim.x, ++local) {
+    for (int t = cid; t < items; t += ncl, ++local) {
       const int buf = local & 1;
       const uint32_t use = local >> 1;
       int l, m0, n0;
-      sched.coords(t, l, m0, n0);
+      sched.coords(t, rank, l, m0, n0);
       const int chunks = sched.half(t) ? BN / 64 : BN / 32;
       mbar_wait(&acc_full[buf], use & 1);
       tc_fence_after();
@@ -187,6 +198,7 @@ gemm_lrelu_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   }
 
   __syncthreads();
+  cluster_sync();  // no multicast or remote arrive may still target this CTA's shared memory
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<TMEM_COLS>(tmem);

@@ -17,7 +17,7 @@ import os
 tgt = AttnTarget(B=int(os.environ.get("AB_B", 4)), H=32, S=int(os.environ.get("AB_S", 4096))).allocate()
 ctx = get_context()
 mods = {k: Module(open(v, 'rb').read(), "attn_fwd_f16", ctx=ctx) for k, v in variants.items()}
-for rnd in range(3):
+for rnd in range(int(os.environ.get("AB_ROUNDS", 3))):
     for k, m in mods.items():
         lp, params = tgt.launch()
         if k in threads:  # the non-persistent layout: (S/256, B*H) grid of 384-thread CTAs
