@@ -41,7 +41,7 @@ int sip_target_gemm_launch(sip_ctx* ctx, const void* A, const void* B, void* C, 
   cuuint32_t ba[3] = {64, 128, 1};
   cuuint64_t db[3] = {(cuuint64_t)K, (cuuint64_t)N, (cuuint64_t)L};
   cuuint64_t sb[2] = {(cuuint64_t)K * 2, (cuuint64_t)N * K * 2};
-  // each CTA of a cluster loads half of the pair's B tile: 128-row boxes for 256-column
+  // each CTA of a pair stages half of the tile's B rows: 128-row boxes for 256-column
   // tiles, 64-row boxes for the 128-column tail halves
   cuuint32_t bb[3] = {64, 128, 1};
   cuuint32_t bh[3] = {64, 64, 1};
@@ -55,8 +55,8 @@ int sip_target_gemm_launch(sip_ctx* ctx, const void* A, const void* B, void* C, 
   std::memcpy(p + 400, &K, 4);
   std::memcpy(p + 404, &L, 4);
   std::memcpy(p + 408, &slope, 4);
-  // persistent clusters of 2 CTAs (tile pairs sharing B), one CTA per SM; problems with at
-  // most half as many pairs as clusters run every pair as two halves (the kernel's Schedule)
+  // persistent CTA pairs (cta_group::2, one 256x256 tile each), one CTA per SM; problems
+  // with at most half as many tiles as pairs run every tile as two halves (the kernel's Schedule)
   long pairs = (long)(M / 256) * (N / 256) * L;
   long cmax = ctx->sm_count / 2;
   long ncl = pairs >= cmax ? cmax : (2 * pairs <= cmax ? 2 * pairs : pairs);
@@ -67,7 +67,7 @@ int sip_target_gemm_launch(sip_ctx* ctx, const void* A, const void* B, void* C, 
   launch->block[1] = launch->block[2] = 1;
   launch->cluster[0] = 2;  // CTA pairs (the kernel reads %cluster_ctarank)
   launch->cluster[1] = launch->cluster[2] = 1;
-  launch->smem_bytes = 4 * (128 * 64 * 2 + 256 * 64 * 2) + 1024 + 256;
+  launch->smem_bytes = 6 * (128 * 64 * 2 + 128 * 64 * 2) + 1024 + 256;  // 6 stages of 32 KB
   launch->params = params;
   launch->param_offsets = kGemmOffsets;
   launch->nparams = 9;

@@ -2,24 +2,27 @@
 //
 // The paper's GEMM+LeakyReLU workload, written by hand for
 // sm_100a instead of Triton/A100:
-//   * persistent clusters of 2 CTAs (one per SM): the pair computes two M-adjacent
-//     128x256 tiles sharing one 256-row B tile; each CTA loads its own A tile and
-//     HALF of B, multicast into both CTAs' shared memory, so a CTA pulls 32 KB per
-//     k-block from L2 instead of 48 KB (the 1-CTA kernel was bound by L2->SM
-//     traffic: its TMA stream alone took 82 of its 102 us at 4096^3);
-//   * static round-robin over tile pairs (batched over L independent problems,
-//     used by the verifier); wave-quantisation tail: when the last round of pairs
-//     would leave more than half the clusters idle (4096^3: 256 pairs on 74
-//     clusters, last wave 46 % full), those pairs run as two 128-column halves
-//     (N=128 MMA, half-height B boxes), so the tail costs half a pair instead of a
-//     full one; problems with at most half as many pairs as clusters run as halves;
-//   * warp 0: TMA producer (SWIZZLE_128B, 4-stage ring: A 16 KB + B 32 KB, of which
-//     this CTA loads 16 KB and the peer the other 16; "empty" needs both CTAs' MMAs);
-//   * warp 1: TMEM allocator + single-thread tcgen05.mma issuer (M128 N256 K16),
-//     accumulating in one of two 256-column TMEM buffers;
+//   * CTA pairs (cta_group::2): a cluster of 2 CTAs computes one 256x256 output tile
+//     with M=256 tcgen05.mma issued by the even CTA.  Each CTA stages only its own
+//     128 rows of A and 128 rows of B (32 KB per k-block) and receives its 128 rows
+//     of the accumulator in its own TMEM; the MMA reads the peer's halves directly.
+//     The 1-CTA kernel was bound by the bytes each SM receives (its TMA stream alone
+//     took 82 of its 102 us at 4096^3 for 48 KB per k-block);
+//   * persistent, static round-robin over 256x256 tiles (batched over L independent
+//     problems, used by the verifier); wave-quantisation tail: when the last round
+//     would leave more than half the pairs idle (4096^3: 256 tiles on 74 pairs, last
+//     wave 46 % full), those tiles run as two 256x128 halves (N=128 MMA), so the
+//     tail costs half a tile; problems with at most half as many tiles as pairs run
+//     as halves throughout;
+//   * warp 0: TMA producer (SWIZZLE_128B, 6-stage ring of 32 KB; both CTAs' loads
+//     complete on the even CTA's "full" barrier, whose producer posts the pair's bytes);
+//   * warp 1: TMEM allocator (cta_group::2) + on the even CTA the single-thread MMA
+//     issuer (M256 N256 K16), accumulating in one of two 256-column TMEM buffers; its
+//     commits multicast to both CTAs ("empty" stages, "accumulator full");
 //   * warps 2-5: epilogue -- tcgen05.ld 32 columns at a time, LeakyReLU in fp32,
-//     pack to fp16, 16-byte st.global per thread; the second TMEM buffer lets
-//     the epilogue of tile i overlap the main loop of tile i+1.
+//     pack to fp16, 16-byte st.global per thread; the second TMEM buffer lets the
+//     epilogue of tile i overlap the main loop of tile i+1; both CTAs' epilogues
+//     release the accumulator on the even CTA's barrier.
 // The epilogue's STG instructions are the global-memory instructions SIP may move
 // under the reference's candidate rules.
 //
@@ -28,14 +31,16 @@
 #include "sm100.cuh"
 
 namespace {
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
-constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 6;
+constexpr int A_BYTES = BM * BK * 2;            // this CTA's 128 rows of A
+constexpr int BH_BYTES = (BN / 2) * BK * 2;     // this CTA's 128 rows of B
+constexpr int STAGE_BYTES = A_BYTES + BH_BYTES;
 constexpr int ACC_COLS = BN, TMEM_COLS = 2 * ACC_COLS;
 constexpr int NUM_THREADS = 192;
-constexpr uint32_t IDESC = sm100::idesc_f16(BM, BN);
-constexpr uint32_t IDESC_HALF = sm100::idesc_f16(BM, BN / 2);
+constexpr uint32_t IDESC = sm100::idesc_f16(2 * BM, BN);
+constexpr uint32_t IDESC_HALF = sm100::idesc_f16(2 * BM, BN / 2);
 
-// Work item t of the cluster's static schedule -> (problem l, m0 of this CTA, n0, half?).
+// Work item t of the pair's static schedule -> (problem l, m0 of this CTA, n0, half?).
 struct Schedule {
   int pairs_m, tiles_n, full, items;
   __device__ Schedule(int M, int N, int L, int nclusters) {
@@ -44,9 +49,9 @@ struct Schedule {
     const int pairs = pairs_m * tiles_n * L;
     const int rem = pairs % nclusters;
     if (2 * pairs <= nclusters) {
-      full = 0;  // few pairs: every pair as two halves
+      full = 0;  // few tiles: every tile as two halves
     } else if (pairs > nclusters && rem != 0 && 2 * rem <= nclusters) {
-      full = pairs - rem;  // whole waves of full pairs, tail as halves
+      full = pairs - rem;  // whole waves of full tiles, tail as halves
     } else {
       full = pairs;
     }
@@ -65,22 +70,24 @@ struct Schedule {
 
 extern "C" __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_lrelu_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-               const __grid_constant__ CUtensorMap tmBh, __half* __restrict__ C, int M, int N, int K, int L, float slope) {
+               const __grid_constant__ CUtensorMap tmBh, __half* __restrict__ C, int M, int N, int K, int L,
+               float slope) {
   using namespace sm100;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);  // used on the even CTA
   uint64_t* empty = full + STAGES;
   uint64_t* acc_full = empty + STAGES;
-  uint64_t* acc_empty = acc_full + 2;
+  uint64_t* acc_empty = acc_full + 2;  // used on the even CTA
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = warp_id();
   const int lane = threadIdx.x & 31;
   const int kblocks = K / BK;
   const int rank = (int)cluster_rank();
+  const bool leader = rank == 0;
   const int cid = (int)cluster_id_x(), ncl = (int)cluster_count_x();
   const Schedule sched(M, N, L, ncl);
   const int items = sched.items;
@@ -91,23 +98,23 @@ gemm_lrelu_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     tma_prefetch(&tmBh);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 2);  // both CTAs' MMAs: each stage's B holds both CTAs' halves
+      mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], 4);
+      mbar_init(&acc_empty[b], 8);  // the 4 epilogue warps of each CTA
     }
     mbar_fence_init();
   }
-  if (warp == 1) tmem_alloc<TMEM_COLS>(tmem_slot);
+  if (warp == 1) tmem_alloc_2sm<TMEM_COLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
-  cluster_sync();  // the peer's barriers are initialised before any multicast lands in them
+  cluster_sync();  // both CTAs' barriers exist before any load or commit targets them
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    // ---------------- TMA producer ----------------
+    // ---------------- TMA producer (both CTAs) ----------------
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
@@ -115,15 +122,13 @@ gemm_lrelu_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         int l, m0, n0;
         sched.coords(t, rank, l, m0, n0);
         const bool half = sched.half(t);
-        const int nb = half ? BN / 2 : BN;        // B rows of the tile
-        const CUtensorMap* mb = half ? &tmBh : &tmB;  // boxes of nb / 2 rows
+        const int nb = half ? BN / 4 : BN / 2;        // this CTA's B rows
+        const CUtensorMap* mb = half ? &tmBh : &tmB;  // boxes of nb rows
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], A_BYTES + nb * BK * 2);
-          tma_load_3d(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, m0, l);
-          // this CTA's half of B, into the same stage of both CTAs
-          tma_load_3d_mc(sB + stage * B_BYTES + rank * (nb / 2) * BK * 2, mb, &full[stage], kb * BK,
-                         n0 + rank * (nb / 2), l, (uint16_t)0x3);
+          if (leader) mbar_expect_tx(&full[stage], 2 * (A_BYTES + nb * BK * 2));  // both CTAs' bytes
+          tma_load_3d_2sm(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, m0, l);
+          tma_load_3d_2sm(sB + stage * BH_BYTES, mb, &full[stage], kb * BK, n0 + rank * nb, l);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -132,37 +137,39 @@ gemm_lrelu_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
-    int stage = 0;
-    uint32_t phase = 0;
-    int local = 0;
-    for (int t = cid; t < items; t += ncl, ++local) {
-      const int buf = local & 1;
-      const uint32_t use = local >> 1;
-      const uint32_t idesc = sched.half(t) ? IDESC_HALF : IDESC;
-      mbar_wait(&acc_empty[buf], (use & 1) ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem + buf * ACC_COLS;
-      for (int kb = 0; kb < kblocks; ++kb) {
-        mbar_wait(&full[stage], phase);
+    // ---------------- MMA issuer (even CTA) ----------------
+    if (leader) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int t = cid; t < items; t += ncl, ++local) {
+        const int buf = local & 1;
+        const uint32_t use = local >> 1;
+        const uint32_t idesc = sched.half(t) ? IDESC_HALF : IDESC;
+        mbar_wait(&acc_empty[buf], (use & 1) ^ 1);
         tc_fence_after();
-        if (elect_one()) {
-          const uint32_t a0 = smem_u32(sA + stage * A_BYTES), b0 = smem_u32(sB + stage * B_BYTES);
+        const uint32_t d_tmem = tmem + buf * ACC_COLS;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t a0 = smem_u32(sA + stage * A_BYTES), b0 = smem_u32(sB + stage * BH_BYTES);
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk)
-            mma_f16(d_tmem, desc_sw128(a0 + kk * 32), desc_sw128(b0 + kk * 32), idesc, (kb | kk) != 0);
-          mma_commit_mc(&empty[stage], (uint16_t)0x3);  // frees the stage in both CTAs
-          if (kb == kblocks - 1) mma_commit(&acc_full[buf]);
-        }
-        __syncwarp();
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
+            for (int kk = 0; kk < BK / 16; ++kk)
+              mma_f16_2sm(d_tmem, desc_sw128(a0 + kk * 32), desc_sw128(b0 + kk * 32), idesc, (kb | kk) != 0);
+            mma_commit_2sm_mc(&empty[stage], (uint16_t)0x3);  // frees the stage in both CTAs
+            if (kb == kblocks - 1) mma_commit_2sm_mc(&acc_full[buf], (uint16_t)0x3);
+          }
+          __syncwarp();
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
       }
     }
   } else {
-    // ---------------- epilogue: warps 2..5 ----------------
+    // ---------------- epilogue: warps 2..5 (both CTAs) ----------------
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int row_in_tile = quarter * 32 + lane;
     int local = 0;
@@ -193,14 +200,19 @@ gemm_lrelu_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+      if (lane == 0) {
+        if (leader)
+          mbar_arrive(&acc_empty[buf]);
+        else
+          mbar_arrive_remote(&acc_empty[buf], 0);
+      }
     }
   }
 
   __syncthreads();
-  cluster_sync();  // no multicast or remote arrive may still target this CTA's shared memory
+  cluster_sync();  // no load, commit or remote arrive may still target either CTA
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<TMEM_COLS>(tmem);
+    tmem_dealloc_2sm<TMEM_COLS>(tmem);
   }
 }
