@@ -30,6 +30,7 @@ struct sip_ctx {
                                      const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                      CUtensorMapL2promotion, CUtensorMapFloatOOBfill) = nullptr;
   CUresult (*cuCtxGetCurrent)(CUcontext*) = nullptr;
+  CUresult (*cuCtxSetCurrent)(CUcontext) = nullptr;
 };
 
 namespace sip {

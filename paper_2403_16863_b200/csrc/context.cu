@@ -47,7 +47,8 @@ int sip_open(int device, sip_ctx** out) {
             resolve("cuLaunchKernelEx", &ctx->cuLaunchKernelEx) &&
             resolve("cuGetErrorString", &ctx->cuGetErrorString) &&
             resolve("cuTensorMapEncodeTiled", &ctx->cuTensorMapEncodeTiled) &&
-            resolve("cuCtxGetCurrent", &ctx->cuCtxGetCurrent);
+            resolve("cuCtxGetCurrent", &ctx->cuCtxGetCurrent) &&
+            resolve("cuCtxSetCurrent", &ctx->cuCtxSetCurrent);
   if (!ok) {
     cudaStreamDestroy(ctx->stream);
     delete ctx;

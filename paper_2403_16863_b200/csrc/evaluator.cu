@@ -106,6 +106,7 @@ struct CachedMod {
   CUfunction fn = nullptr;
   uint32_t smem_set = 0;
   uint64_t stamp = 0;
+  bool pinned = false;  // in use by the batch being measured: never evicted
 };
 
 }  // namespace
@@ -171,6 +172,16 @@ int cu_fail(sip_ctx* ctx, int code, const char* what, CUresult r) {
   return sip::fail(ctx, code, std::string(what) + ": " + (s ? s : "CUDA driver error"));
 }
 
+// unload the least recently used module that no batch in flight is holding
+void evict_one(sip_module* m) {
+  auto victim = m->cache.end();
+  for (auto it = m->cache.begin(); it != m->cache.end(); ++it)
+    if (!it->pinned && (victim == m->cache.end() || it->stamp < victim->stamp)) victim = it;
+  if (victim == m->cache.end()) return;
+  m->ctx->cuModuleUnload(victim->mod);
+  m->cache.erase(victim);
+}
+
 int get_module(sip_module* m, const uint16_t* perm, CachedMod** out) {
   std::vector<uint16_t> key;
   if (perm) key.assign(perm, perm + m->n);
@@ -194,12 +205,7 @@ int get_module(sip_module* m, const uint16_t* perm, CachedMod** out) {
     return cu_fail(ctx, SIP_E_MEASURE, "cuModuleGetFunction", r);
   }
   cm.stamp = ++m->clock;
-  if (m->cache.size() >= m->cache_cap) {
-    auto victim = std::min_element(m->cache.begin(), m->cache.end(),
-                                   [](const CachedMod& a, const CachedMod& b) { return a.stamp < b.stamp; });
-    ctx->cuModuleUnload(victim->mod);
-    m->cache.erase(victim);
-  }
+  if (m->cache.size() >= m->cache_cap) evict_one(m);
   m->cache.push_back(cm);
   *out = &m->cache.back();
   return SIP_OK;
@@ -485,18 +491,35 @@ int sip_measure_paired(sip_module* m, const uint16_t* perm_ref, const uint16_t* 
 // every candidate's (warmup + reps) interleaved pairs with the baseline run from ONE
 // CUDA graph, so the GPU does not idle between candidates for loads, graph builds and
 // host round trips.  status[i] = SIP_OK or SIP_E_MEASURE (that candidate is skipped).
+static int measure_batch_impl(sip_module* m, const uint16_t* perm_ref, const uint16_t* perms, int32_t k,
+                              const sip_launch* L, int32_t warmup, int32_t reps, int32_t flush_l2,
+                              double* ratio_median, double* ref_median_ms, double* cand_median_ms,
+                              double* raw_ratio, int32_t* status);
+
 int sip_measure_paired_batch(sip_module* m, const uint16_t* perm_ref, const uint16_t* perms, int32_t k,
                              const sip_launch* L, int32_t warmup, int32_t reps, int32_t flush_l2,
                              double* ratio_median, double* ref_median_ms, double* cand_median_ms,
                              double* raw_ratio, int32_t* status) {
   if (!m || !L || !m->ctx || !perms || k < 1 || !ratio_median || !status || reps < 1 || warmup < 0)
     return SIP_E_ARG;
+  const int rc = measure_batch_impl(m, perm_ref, perms, k, L, warmup, reps, flush_l2, ratio_median,
+                                    ref_median_ms, cand_median_ms, raw_ratio, status);
+  for (auto& c : m->cache) c.pinned = false;  // the batch's modules may be evicted again
+  return rc;
+}
+
+}  // extern "C"
+
+static int measure_batch_impl(sip_module* m, const uint16_t* perm_ref, const uint16_t* perms, int32_t k,
+                              const sip_launch* L, int32_t warmup, int32_t reps, int32_t flush_l2,
+                              double* ratio_median, double* ref_median_ms, double* cand_median_ms,
+                              double* raw_ratio, int32_t* status) {
   sip_ctx* ctx = m->ctx;
   if (m->cache_cap < (size_t)k + 1) m->cache_cap = (size_t)k + 1;
   CachedMod* ref = nullptr;
   int rc = get_module(m, perm_ref, &ref);
   if (rc != SIP_OK) return rc;
-  ref->stamp = ~0ull >> 1;  // the baseline is reused by every batch: never the eviction victim
+  ref->pinned = true;  // held by every pair of this batch
   // images + parallel cuModuleLoadData for the candidates not loaded yet
   std::vector<CachedMod*> mods(k, nullptr);
   std::vector<int> todo;
@@ -506,6 +529,7 @@ int sip_measure_paired_batch(sip_module* m, const uint16_t* perm_ref, const uint
     for (auto& c : m->cache)
       if (c.perm == key) {
         c.stamp = ++m->clock;
+        c.pinned = true;
         mods[i] = &c;
       }
     status[i] = SIP_OK;
@@ -516,13 +540,23 @@ int sip_measure_paired_batch(sip_module* m, const uint16_t* perm_ref, const uint
   std::vector<CUresult> lres(todo.size(), CUDA_SUCCESS);
   for (size_t t = 0; t < todo.size(); ++t)
     if (build_image(m, perms + (size_t)todo[t] * m->n, imgs[t]) != SIP_OK) lres[t] = CUDA_ERROR_INVALID_IMAGE;
-  const int nthreads = (int)std::min<size_t>(todo.size(), 8);
+  // the loads run in this thread's CUDA context (made current in each worker), so the
+  // modules belong to the context the launches below use
+  CUcontext cur = nullptr;
+  if (ctx->cuCtxGetCurrent(&cur) != CUDA_SUCCESS || cur == nullptr) {
+    SIP_CUDA(ctx, cudaFree(nullptr));  // bind this device's primary context
+    ctx->cuCtxGetCurrent(&cur);
+  }
+  const char* lt = getenv("SIP_LOAD_THREADS");
+  const int want = lt ? std::max(1, atoi(lt)) : 8;
+  const int nthreads = (int)std::min<size_t>(todo.size(), (size_t)want);
   std::vector<std::thread> pool;
   for (int w = 0; w < nthreads; ++w)
     pool.emplace_back([&, w]() {
-      cudaSetDevice(ctx->device);  // make the primary context current in this thread
+      const bool ctx_ok = ctx->cuCtxSetCurrent(cur) == CUDA_SUCCESS;
       for (size_t t = w; t < todo.size(); t += nthreads)
-        if (lres[t] == CUDA_SUCCESS) lres[t] = ctx->cuModuleLoadData(&loaded[t], imgs[t].data());
+        if (lres[t] == CUDA_SUCCESS)
+          lres[t] = ctx_ok ? ctx->cuModuleLoadData(&loaded[t], imgs[t].data()) : CUDA_ERROR_INVALID_CONTEXT;
     });
   for (auto& th : pool) th.join();
   for (size_t t = 0; t < todo.size(); ++t) {
@@ -540,12 +574,8 @@ int sip_measure_paired_batch(sip_module* m, const uint16_t* perm_ref, const uint
       continue;
     }
     cm.stamp = ++m->clock;
-    while (m->cache.size() >= m->cache_cap) {  // evict the oldest, never this batch's
-      auto victim = std::min_element(m->cache.begin(), m->cache.end(),
-                                     [](const CachedMod& a, const CachedMod& b) { return a.stamp < b.stamp; });
-      ctx->cuModuleUnload(victim->mod);
-      m->cache.erase(victim);
-    }
+    cm.pinned = true;
+    if (m->cache.size() >= m->cache_cap) evict_one(m);  // the oldest module not in this batch
     m->cache.push_back(cm);
     mods[i] = &m->cache.back();
   }
@@ -606,5 +636,3 @@ int sip_measure_paired_batch(sip_module* m, const uint16_t* perm_ref, const uint
     return sip::fail(ctx, SIP_E_MEASURE, std::string("timed launches: ") + cudaGetErrorString(ce));
   return SIP_OK;
 }
-
-}  // extern "C"

@@ -203,3 +203,32 @@ def test_measure_batch_paired():
     for smp in out:
         assert smp.unit == "ms" and len(smp.raw) == 5
         assert 0.8 * be.ref_ms < smp.value < 1.25 * be.ref_ms
+
+
+def test_measure_batch_module_cache_churn():
+    """Batches larger than the module cache, repeated, with the baseline schedule itself
+    among the candidates: no module a batch still launches may be evicted (a dangling
+    handle showed up as 'invalid resource handle')."""
+    from paper_2403_16863_b200.tables import movable_in
+
+    tgt = GemmTarget(M=512, N=512, K=512).allocate()
+    be = B200Backend(tgt)
+    seq = be.kernel.schedule
+    n = len(seq)
+    dk = be.ctx.kernel(be.tables_for(be.kernel, "extended"))
+    ident = np.arange(n, dtype=np.uint16)
+    los = [lo for lo in range(n - 1)
+           if movable_in(seq[lo], "extended") or movable_in(seq[lo + 1], "extended")]
+    legal = np.asarray(los)[dk.legality(np.tile(ident, (len(los), 1)), los, hw_safe=True,
+                                        min_fixed=be.min_fixed).astype(bool)]
+    swaps = []
+    for lo in legal[:10]:
+        p = ident.copy()
+        p[lo], p[lo + 1] = p[lo + 1], p[lo]
+        swaps.append(p)
+    assert len(swaps) >= 4
+    for r in range(3):
+        batch = [ident] + swaps[r % len(swaps):] + [ident] + swaps[: r % len(swaps)]
+        out = be.measure_batch(np.stack(batch), reps=3)
+        assert all(not isinstance(o, Exception) for o in out)
+        assert all(0.7 * be.ref_ms < o.value < 1.4 * be.ref_ms for o in out)
