@@ -68,7 +68,42 @@ CANDIDATE_CLASSES = {
 # wait mask is an acquire point no move crosses (csrc/engine.cu hw_safe_ok).
 SIMPLE_COMPUTE = frozenset(
     "FFMA FMUL FADD FMNMX FSEL FSETP FSET IADD3 IMAD LOP3 SHF MOV SEL ISETP PRMT LEA F2FP "
-    "HFMA2 HADD2 HMUL2 IABS IMNMX VIADD VIMNMX".split())
+    "HFMA2 HADD2 HMUL2 IABS IMNMX VIADD VIMNMX FMNMX3 FFMA2 FADD2 FMUL2".split())
+# sm_100a packed fp32 pairs: the destination and every ".F32x2" source name a 64-bit
+# register pair R(n):R(n+1); ".F32" sources are scalar broadcasts.  The reference's model
+# sees one register per operand, so the extension widens these before building tables.
+PAIR_OPS = frozenset(("FFMA2", "FADD2", "FMUL2"))
+
+
+def _next_reg(name: str) -> str | None:
+    m = re.match(r"^(U?R)(\d+)$", name)
+    return None if m is None else f"{m.group(1)}{int(m.group(2)) + 1}"
+
+
+_NULL = frozenset(("RZ", "URZ", "PT", "UPT"))
+# unknown to the reference's class table (class OTHER: every register read and written),
+# modelled exactly by the extension: one destination, the rest sources
+EXACT_OPS = PAIR_OPS | {"FMNMX3"}
+
+
+def extension_reads_writes(ins, rw):
+    """Exact footprint of the sm_100a compute instructions the extension moves; any
+    other instruction keeps the reference's (deps.reads_writes) sets."""
+    if ins.base_mnemonic not in EXACT_OPS:
+        return rw
+    reads, writes = set(), set()
+    if ins.predicate:
+        reads.add(ins.predicate)
+    pair = ins.base_mnemonic in PAIR_OPS
+    for k, op in enumerate(ins.operands):
+        if op.reg is None or op.kind not in (OperandKind.REGISTER, OperandKind.PREDICATE):
+            continue
+        names = {op.reg}
+        hi = _next_reg(op.reg) if op.kind is OperandKind.REGISTER else None
+        if pair and hi is not None and (k == 0 or "F32x2" in op.text):
+            names.add(hi)
+        (writes if k == 0 else reads).update(names)
+    return frozenset(reads - _NULL), frozenset(writes - _NULL)
 _WIDE_MODS = frozenset(("64", "WIDE", "128", "U64", "S64", "F64", "X"))
 
 
@@ -94,7 +129,8 @@ def hw_simple(ins) -> bool:
 def movable_in(ins, classes: str) -> bool:
     if classes == "global":
         return ins.klass in GLOBAL_CLASSES
-    return ins.klass in GLOBAL_CLASSES or (ins.klass in CANDIDATE_CLASSES[classes] and hw_simple(ins))
+    return ins.klass in GLOBAL_CLASSES or (
+        (ins.klass in CANDIDATE_CLASSES[classes] or ins.base_mnemonic in EXACT_OPS) and hw_simple(ins))
 
 
 _LONG_REG = re.compile(r"^U?P[0-6]$|^UR\d+$")  # predicates and uniform registers
@@ -156,6 +192,8 @@ class KernelTables:
             return intern[name]
 
         rw = [reads_writes(ins) for ins in sched]
+        if classes != "global":  # hardware-mode extension: exact footprints of packed pairs
+            rw = [extension_reads_writes(ins, x) for ins, x in zip(sched, rw)]
         for r, w in rw:
             for name in sorted(r | w):
                 rid(name)
