@@ -17,8 +17,14 @@ import os
 tgt = AttnTarget(B=int(os.environ.get("AB_B", 4)), H=32, S=int(os.environ.get("AB_S", 4096))).allocate()
 ctx = get_context()
 mods = {k: Module(open(v, 'rb').read(), "attn_fwd_f16", ctx=ctx) for k, v in variants.items()}
-for rnd in range(int(os.environ.get("AB_ROUNDS", 3))):
-    for k, m in mods.items():
+import statistics
+res = {k: [] for k in mods}
+names = list(mods)
+rounds = int(os.environ.get("AB_ROUNDS", 3))
+for rnd in range(rounds):
+    order = names[rnd % len(names):] + names[: rnd % len(names)]  # rotate: no variant always last
+    for k in order:
+        m = mods[k]
         lp, params = tgt.launch()
         if k in threads:  # the non-persistent layout: (S/256, B*H) grid of 384-thread CTAs
             lp.block[0] = threads[k]
@@ -27,4 +33,9 @@ for rnd in range(int(os.environ.get("AB_ROUNDS", 3))):
         med = ctypes.c_double(); raw = np.zeros(10)
         ctx.check(ctx.lib.sip_measure(m.handle, None, ctypes.byref(lp), 2, 10, 0, ctypes.byref(med),
                                       raw.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
-        print(f"{k:20s} {med.value*1e3:8.1f} us  {tgt.flops/med.value/1e9:7.1f} TFLOP/s", flush=True)
+        res[k].append(tgt.flops / med.value / 1e9)
+        if rounds <= 3:
+            print(f"{k:20s} {med.value*1e3:8.1f} us  {tgt.flops/med.value/1e9:7.1f} TFLOP/s", flush=True)
+for k in names:
+    print(f"{k:20s} median over {rounds} rounds: {statistics.median(res[k]):7.1f} TFLOP/s "
+          f"(min {min(res[k]):.0f}, max {max(res[k]):.0f})", flush=True)
