@@ -331,6 +331,61 @@ __device__ Staged stage_tables(const KernelDev& d, bool use_smem) {
   return {m, g};
 }
 
+// init_by_array (CPython's seeding, rng.cuh) for an int seed (<= 2 key words) into one
+// chain-major row of 624 words, eight words per pair of 16-byte accesses: the serial
+// mixing chain stays in registers and every access moves a whole 32-byte sector.
+__device__ void mt_seed_row(uint32_t* row, const uint32_t* __restrict__ base, const uint32_t* key, int klen) {
+  uint4* r4 = reinterpret_cast<uint4*>(row);
+  // pass 1, i = 1..623: v_i = (base_i ^ f1(v_{i-1})) + key_j + j
+  uint32_t prev = base[0];
+  int j = 0;
+  for (int q = 0; q < MT_N / 8; ++q) {
+    uint32_t w[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = q * 8 + u;
+      if (i == 0) {
+        w[u] = 0u;  // slot 0 is set after the pass (CPython copies word 623 there)
+        continue;
+      }
+      const uint32_t v = (__ldg(base + i) ^ ((prev ^ (prev >> 30)) * 1664525u)) + key[j] + (uint32_t)j;
+      w[u] = v;
+      prev = v;
+      if (++j >= klen) j = 0;
+    }
+    r4[2 * q] = make_uint4(w[0], w[1], w[2], w[3]);
+    r4[2 * q + 1] = make_uint4(w[4], w[5], w[6], w[7]);
+  }
+  // wrap: mt[0] = mt[623]; the pass's 624th step revisits i = 1
+  row[0] = prev;
+  {
+    const uint32_t v = (row[1] ^ ((prev ^ (prev >> 30)) * 1664525u)) + key[j] + (uint32_t)j;
+    row[1] = v;
+    prev = v;
+  }
+  // pass 2, i = 2..623: v_i = (v'_i ^ f2(v_{i-1})) - i
+  for (int q = 0; q < MT_N / 8; ++q) {
+    const uint4 a = r4[2 * q], b = r4[2 * q + 1];
+    uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = q * 8 + u;
+      if (i < 2) continue;
+      const uint32_t v = (w[u] ^ ((prev ^ (prev >> 30)) * 1566083941u)) - (uint32_t)i;
+      w[u] = v;
+      prev = v;
+    }
+    r4[2 * q] = make_uint4(w[0], w[1], w[2], w[3]);
+    r4[2 * q + 1] = make_uint4(w[4], w[5], w[6], w[7]);
+  }
+  // wrap again: mt[0] = mt[623]; the pass's last step is i = 1; then mt[0] = 0x80000000
+  {
+    const uint32_t v = (row[1] ^ ((prev ^ (prev >> 30)) * 1566083941u)) - 1u;
+    row[1] = v;
+  }
+  row[0] = 0x80000000u;
+}
+
 __device__ void chain_init(const KernelDev& d, const int16_t* gid, const Chains& s, int c,
                            const uint32_t* base, MtRef& mt) {
   // rows written 8 positions per 16-byte store; candidate lookups from the staged table
@@ -351,8 +406,9 @@ __device__ void chain_init(const KernelDev& d, const int16_t* gid, const Chains&
     brow[q] = v;
   }
   uint32_t key[2];
-  int klen = mt_key_from_int(s.seeds[c], key);
-  mt_init_by_array(mt, base, key, klen);
+  const int klen = mt_key_from_int(s.seeds[c], key);
+  mt_seed_row(mt.st, base, key, klen);  // chain-major row (MtRef stride 1)
+  mt.mti = MT_N;
 }
 
 // ---- checkpointed scoreboard replay -----------------------------------------
@@ -519,7 +575,7 @@ __global__ void __launch_bounds__(128) anneal_fused_kernel(KernelDev d, Chains s
   Staged tb = stage_tables(d, use_smem);
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= s.C) return;
-  MtRef mt{s.mt + c, s.C, MT_N};
+  MtRef mt{s.mt + (size_t)c * MT_N, 1, MT_N};  // chain-major: a chain's draws stay in its own sectors
   chain_init(d, tb.gid, s, c, mt_base, mt);
   const double t0 = t0_cycles;
   int total_x = ck_copy_start(s, c);
@@ -582,7 +638,7 @@ __global__ void chains_init_kernel(KernelDev d, Chains s, const uint32_t* mt_bas
                                    const double* t0) {
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= s.C) return;
-  MtRef mt{s.mt + c, s.C, MT_N};
+  MtRef mt{s.mt + (size_t)c * MT_N, 1, MT_N};  // chain-major: a chain's draws stay in its own sectors
   chain_init(d, d.gid, s, c, mt_base, mt);
   s.mti[c] = mt.mti;
   s.t0[c] = t0[c];
@@ -599,7 +655,7 @@ __global__ void __launch_bounds__(128) chains_propose_kernel(KernelDev d, Chains
   Staged tb = stage_tables(d, use_smem);
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= s.C) return;
-  MtRef mt{s.mt + c, s.C, s.mti[c]};
+  MtRef mt{s.mt + (size_t)c * MT_N, 1, s.mti[c]};
   int it = s.it[c];
   int lo = -1, cand = 0, dir = 0;
   while (it < s.budget) {
@@ -640,7 +696,7 @@ __global__ void chains_resolve_kernel(KernelDev d, Chains s, const double* t_cur
     record(s, c, it, st, 0.0, lo, cand, dir);
     return;
   }
-  MtRef mt{s.mt + c, s.C, s.mti[c]};
+  MtRef mt{s.mt + (size_t)c * MT_N, 1, s.mti[c]};
   double t = t_curr[c], t0 = s.t0[c];
   double e_c = t / t0, e_x = s.e_x[c];
   double de = e_c - e_x;
