@@ -95,3 +95,26 @@ def test_b200_external_adapter(tmp_path):
     f = tmp_path / "x.sass"
     f.write_text(serialize_kernel(listing.kernel))
     assert main(["measure", str(f), "--shape", "M=512,N=512,K=2048", "--reps", "2"]) == 0
+
+
+def test_optimize_b200_emits_patched_cubin(tmp_path, capsys):
+    """`optimize --backend b200:gemm` on the decoded listing of the shipped cubin: the
+    store gets best.sass and best.cubin, whose kernel words are a permutation of the
+    original's (the emitted schedule as a loadable binary)."""
+    import numpy as np
+
+    from paper_2403_16863_b200.cubin import Module
+    from paper_2403_16863_b200.targets import TARGET_DIR
+
+    cub = TARGET_DIR / "gemm_lrelu.cubin"
+    lst = tmp_path / "gemm.sass"
+    assert main(["decode", str(cub), "gemm_lrelu_f16", "-o", str(lst)]) == 0
+    rc = main(["optimize", str(lst), "--backend", "b200:gemm", "--chains", "2", "--store", str(tmp_path / "st")])
+    out = capsys.readouterr().out
+    assert rc == 0, out
+    run = [p for p in (tmp_path / "st").iterdir() if p.is_dir()][0]
+    assert (run / "best.sass").exists() and (run / "best.cubin").exists()
+    w0 = Module(cub.read_bytes(), "gemm_lrelu_f16").words()
+    w1 = Module((run / "best.cubin").read_bytes(), "gemm_lrelu_f16").words()
+    key = lambda w: sorted(map(tuple, w.tolist()))  # noqa: E731
+    assert key(w0) == key(w1)

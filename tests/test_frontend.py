@@ -72,3 +72,30 @@ def test_classify_table():
     assert classify("UTMALDG.2D") is InstrClass.OTHER  # K6: TMA is OTHER under reference rules
     assert classify("BAR.SYNC") is InstrClass.BARRIER
     assert ControlCode().to_text() == "[B------:R-:W-:-:S01]"
+
+
+def test_cli_patch_roundtrip(tmp_path):
+    """`patch` writes a cubin whose kernel section follows a listing's schedule: the
+    identity listing reproduces the cubin, a swapped listing swaps the two 16-byte words."""
+    from paper_2403_16863_b200.cli import main
+    from paper_2403_16863_b200.cubin import Module, render_listing
+    from paper_2403_16863_b200.ir import Kernel
+    from paper_2403_16863_b200.sasstext import serialize_kernel
+    from paper_2403_16863_b200.targets import TARGET_DIR
+
+    cub = TARGET_DIR / "gemm_lrelu.cubin"
+    L = render_listing(cub.read_bytes(), "gemm_lrelu_f16")
+    ident = tmp_path / "ident.sass"
+    ident.write_text(L.text)
+    out = tmp_path / "out.cubin"
+    assert main(["patch", str(cub), "gemm_lrelu_f16", str(ident), "-o", str(out)]) == 0
+    m0 = Module(cub.read_bytes(), "gemm_lrelu_f16")
+    m1 = Module(out.read_bytes(), "gemm_lrelu_f16")
+    assert (m0.words() == m1.words()).all()
+    sched = list(L.kernel.schedule)
+    sched[10], sched[11] = sched[11], sched[10]
+    sw = tmp_path / "swap.sass"
+    sw.write_text(serialize_kernel(Kernel(name="k", schedule=tuple(sched))))
+    assert main(["patch", str(cub), "gemm_lrelu_f16", str(sw), "-o", str(out)]) == 0
+    w0, w1 = m0.words(), Module(out.read_bytes(), "gemm_lrelu_f16").words()
+    assert (w1[10] == w0[11]).all() and (w1[11] == w0[10]).all() and (w1[12:] == w0[12:]).all()
