@@ -250,6 +250,8 @@ struct Chains {
   int32_t* ckpt = nullptr;          // [nck][8][C] state of the current schedule
   int32_t* ckpt2 = nullptr;         // [nck][8][C] state of the candidate being priced
   int32_t* ck0 = nullptr;           // [nck][8] + total: checkpoints of the start schedule
+  uint16_t* row0 = nullptr;         // [ns] the start schedule (zero-padded)
+  uint16_t* cpos0 = nullptr;        // [k] candidate positions in the start schedule
   uint16_t* acclog = nullptr;       // [budget][C] lo of every accepted swap (fused kernel)
   int64_t* replayed = nullptr;      // [C] scoreboard steps executed (instrumentation)
   int32_t* priced = nullptr;        // [C] priced iterations
@@ -547,7 +549,14 @@ __device__ void ck_commit(const Chains& s, int c, int lo, int jconv, int delta) 
 // Every chain of a launch starts from the same schedule, so its checkpoints are
 // computed once (one thread) and copied by each chain instead of replayed n times.
 __global__ void start_ckpt_kernel(KernelDev d, Chains s) {
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  if (blockIdx.x != 0) return;
+  for (int p = threadIdx.x; p < s.ns; p += blockDim.x)
+    s.row0[p] = p < s.n ? (s.start ? s.start[p] : (uint16_t)p) : (uint16_t)0;
+  if (threadIdx.x != 0) return;
+  for (int p = 0, j = 0; p < s.n; ++p) {
+    const uint16_t x = s.start ? s.start[p] : (uint16_t)p;
+    if (d.gid[x] >= 0) s.cpos0[j++] = (uint16_t)p;
+  }
   Sb st;
   st.reset();
   for (int j = 0; j < s.nck; ++j) {
@@ -561,24 +570,46 @@ __global__ void start_ckpt_kernel(KernelDev d, Chains s) {
   s.ck0[(size_t)s.nck * 8] = st.total();
 }
 
-__device__ int ck_copy_start(const Chains& s, int c) {
-  const int4* src = reinterpret_cast<const int4*>(s.ck0);
-  int4* dst = ck_at(s.ckpt, s, c, 0);
-  for (int q = 0; q < 2 * s.nck; ++q) dst[q] = src[q];
-  return s.ck0[(size_t)s.nck * 8];
-}
 
 // ---- fused simulator-energy annealing: whole chain in one launch ----------
 __global__ void __launch_bounds__(128) anneal_fused_kernel(KernelDev d, Chains s,
                                                            const uint32_t* mt_base, int use_smem,
                                                            double t0_cycles) {
   Staged tb = stage_tables(d, use_smem);
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  {
+    // every chain starts from the same schedule: the warp writes its 32 chains' rows and
+    // checkpoints cooperatively, lane-consecutive 16-byte pieces of one chain at a time,
+    // so each store fills whole 128-byte lines (per-lane row writes scattered 32 rows
+    // per instruction and made initialisation a fifth of the launch)
+    const int lane = threadIdx.x & 31, cw = c - lane;
+    const uint4* r0 = reinterpret_cast<const uint4*>(s.row0);
+    const int4* k0 = reinterpret_cast<const int4*>(s.ck0);
+    const int nq = s.ns / 8, nk = 2 * s.nck;
+    for (int k = 0; k < 32 && cw + k < s.C; ++k) {
+      uint4* sr = reinterpret_cast<uint4*>(s.sched + (size_t)(cw + k) * s.ns);
+      uint4* br = reinterpret_cast<uint4*>(s.best + (size_t)(cw + k) * s.ns);
+      for (int q = lane; q < nq; q += 32) {
+        const uint4 v = r0[q];
+        sr[q] = v;
+        br[q] = v;
+      }
+      int4* ck = ck_at(s.ckpt, s, cw + k, 0);
+      for (int q = lane; q < nk; q += 32) ck[q] = k0[q];
+    }
+    __syncwarp();  // the rows a lane reads below were written by its warp-mates
+  }
   if (c >= s.C) return;
+  for (int j = 0; j < s.k; ++j) s.cpos[(size_t)j * s.C + c] = s.cpos0[j];
   MtRef mt{s.mt + (size_t)c * MT_N, 1, MT_N};  // chain-major: a chain's draws stay in its own sectors
-  chain_init(d, tb.gid, s, c, mt_base, mt);
+  {
+    uint32_t key[2];
+    const int klen = mt_key_from_int(s.seeds[c], key);
+    mt_seed_row(mt.st, mt_base, key, klen);
+    mt.mti = MT_N;
+  }
   const double t0 = t0_cycles;
-  int total_x = ck_copy_start(s, c);
+  int total_x = s.ck0[(size_t)s.nck * 8];
   int64_t steps = 0;  // scoreboard steps replayed by this chain (the start replay is shared)
   double e_x = (double)total_x / t0, e_best = e_x;
   int best_iter = -1, amb = 0, priced = 0, nacc = 0, best_nacc = 0;
@@ -877,6 +908,8 @@ static int chains_alloc(sip_ctx* ctx, sip_kernel* k, const sip_anneal_cfg* cfg, 
   TRY(dalloc(ctx, &s.ckpt, (size_t)s.nck * 8 * C));
   TRY(dalloc(ctx, &s.ckpt2, (size_t)s.nck * 8 * C));
   TRY(dalloc(ctx, &s.ck0, (size_t)s.nck * 8 + 4));
+  TRY(dalloc(ctx, &s.row0, (size_t)s.ns));
+  TRY(dalloc(ctx, &s.cpos0, (size_t)std::max(s.k, 1)));
   TRY(dalloc(ctx, &s.acclog, (size_t)std::max(s.budget, 1) * C));
   TRY(dalloc(ctx, &s.replayed, C));
   TRY(dalloc(ctx, &s.priced, C));
@@ -898,7 +931,7 @@ static void chains_free(sip_chains* o) {
   void* ptrs[] = {s.sched, s.best, s.cpos, s.mt, s.mti, s.t0, s.e_x, s.e_best, s.it,
                   s.best_iter, s.ambiguous, s.p_lo, s.p_cand, s.p_dir, s.hist, o->d_temps,
                   o->d_seeds, o->d_tcurr, o->d_status, o->d_lo, s.cand_out, o->d_adopt,
-                  s.ckpt, s.ckpt2, s.ck0, s.acclog, s.replayed, s.priced, o->d_start};
+                  s.ckpt, s.ckpt2, s.ck0, s.row0, s.cpos0, s.acclog, s.replayed, s.priced, o->d_start};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
