@@ -1266,52 +1266,59 @@ int sip_anneal_ex(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds
 
 }  // extern "C"
 
-// One block reduces a launch to the epoch record: the champion under the reference's
-// ranking (best energy, then seed; driver.py:81-85) and the instrumentation sums.
-__global__ void __launch_bounds__(1024) epoch_reduce_kernel(Chains s, sip_epoch_result* out) {
-  __shared__ double se[1024];
-  __shared__ int64_t ss[1024], sp[1024], sr[1024], sa[1024];
-  __shared__ int sc[1024];
-  const int t = threadIdx.x;
-  double be = INFINITY;
-  int64_t bs = INT64_MAX, pri = 0, rep = 0, amb = 0;
-  int bc = -1;
-  for (int c = t; c < s.C; c += blockDim.x) {
-    const double e = s.e_best[c];
-    const int64_t sd = s.seeds[c];
-    if (e < be || (e == be && sd < bs)) {
-      be = e;
-      bs = sd;
-      bc = c;
-    }
-    pri += s.priced[c];
-    rep += s.replayed[c];
-    amb += s.ambiguous[c];
+// The epoch record: the champion under the reference's ranking (best energy, then seed;
+// driver.py:81-85) and the instrumentation sums.  Pass 1: a grid of blocks, each reducing
+// a strided slice of the chains into partial[block]; pass 2: one block over the partials.
+struct EpochAcc {
+  double e;
+  int64_t seed, pri, rep, amb;
+  int c;
+};
+__device__ __forceinline__ void epoch_merge(EpochAcc& a, const EpochAcc& b) {
+  if (b.c >= 0 && (a.c < 0 || b.e < a.e || (b.e == a.e && b.seed < a.seed))) {
+    a.e = b.e;
+    a.seed = b.seed;
+    a.c = b.c;
   }
-  se[t] = be, ss[t] = bs, sc[t] = bc, sp[t] = pri, sr[t] = rep, sa[t] = amb;
+  a.pri += b.pri;
+  a.rep += b.rep;
+  a.amb += b.amb;
+}
+__device__ void epoch_block_reduce(EpochAcc v, sip_epoch_result* out) {
+  __shared__ EpochAcc sh[256];
+  const int t = threadIdx.x;
+  sh[t] = v;
   __syncthreads();
   for (int h = blockDim.x / 2; h > 0; h >>= 1) {
-    if (t < h) {
-      const int u = t + h;
-      if (sc[u] >= 0 && (sc[t] < 0 || se[u] < se[t] || (se[u] == se[t] && ss[u] < ss[t]))) {
-        se[t] = se[u];
-        ss[t] = ss[u];
-        sc[t] = sc[u];
-      }
-      sp[t] += sp[u];
-      sr[t] += sr[u];
-      sa[t] += sa[u];
-    }
+    if (t < h) epoch_merge(sh[t], sh[t + h]);
     __syncthreads();
   }
   if (t == 0) {
-    out->champion_chain = sc[0];
-    out->best_energy = se[0];
-    out->best_seed = ss[0];
-    out->priced = sp[0];
-    out->replayed = sr[0];
-    out->ambiguous = sa[0];
+    out->champion_chain = sh[0].c;
+    out->best_energy = sh[0].e;
+    out->best_seed = sh[0].seed;
+    out->priced = sh[0].pri;
+    out->replayed = sh[0].rep;
+    out->ambiguous = sh[0].amb;
   }
+}
+__global__ void __launch_bounds__(256) epoch_partial_kernel(Chains s, sip_epoch_result* partial) {
+  EpochAcc a{INFINITY, INT64_MAX, 0, 0, 0, -1};
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < s.C; c += gridDim.x * blockDim.x) {
+    const EpochAcc b{s.e_best[c], s.seeds[c], (int64_t)s.priced[c], s.replayed[c], (int64_t)s.ambiguous[c], c};
+    epoch_merge(a, b);
+  }
+  epoch_block_reduce(a, partial + blockIdx.x);
+}
+__global__ void __launch_bounds__(256) epoch_final_kernel(const sip_epoch_result* partial, int np,
+                                                          sip_epoch_result* out) {
+  EpochAcc a{INFINITY, INT64_MAX, 0, 0, 0, -1};
+  for (int i = threadIdx.x; i < np; i += blockDim.x) {
+    const sip_epoch_result& r = partial[i];
+    const EpochAcc b{r.best_energy, r.best_seed, r.priced, r.replayed, r.ambiguous, r.champion_chain};
+    epoch_merge(a, b);
+  }
+  epoch_block_reduce(a, out);
 }
 
 extern "C" {
@@ -1323,13 +1330,16 @@ int sip_anneal_epoch(sip_kernel* k, const sip_anneal_cfg* cfg, int64_t seed_base
   if (rc != SIP_OK) return rc;
   sip_ctx* ctx = k->ctx;
   sip_chains& o = *k->ws;
+  constexpr int kParts = 256;
   if (!k->d_epoch) {
     sip_epoch_result* p = nullptr;
-    TRY(dalloc(ctx, &p, 1));
+    TRY(dalloc(ctx, &p, 1 + kParts));
     k->d_epoch = p;
   }
   sip_epoch_result* d_res = static_cast<sip_epoch_result*>(k->d_epoch);
-  epoch_reduce_kernel<<<1, 1024, 0, ctx->stream>>>(o.s, d_res);
+  const int np = std::min(kParts, std::max(1, ctx->sm_count));
+  epoch_partial_kernel<<<np, 256, 0, ctx->stream>>>(o.s, d_res + 1);
+  epoch_final_kernel<<<1, 256, 0, ctx->stream>>>(d_res + 1, np, d_res);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaMemcpyAsync(result, d_res, sizeof *result, cudaMemcpyDeviceToHost, ctx->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
