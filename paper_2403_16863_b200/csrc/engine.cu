@@ -548,10 +548,13 @@ __device__ void ck_commit(const Chains& s, int c, int lo, int jconv, int delta) 
 
 // Every chain of a launch starts from the same schedule, so its checkpoints are
 // computed once (one thread) and copied by each chain instead of replayed n times.
-__global__ void start_ckpt_kernel(KernelDev d, Chains s) {
+__global__ void start_ckpt_kernel(KernelDev d, Chains s, int use_smem) {
   if (blockIdx.x != 0) return;
+  // the serial replay below reads the (ctrl, latency) table staged in shared memory
+  Staged tb = stage_tables(d, use_smem);
   for (int p = threadIdx.x; p < s.ns; p += blockDim.x)
     s.row0[p] = p < s.n ? (s.start ? s.start[p] : (uint16_t)p) : (uint16_t)0;
+  __syncthreads();
   if (threadIdx.x != 0) return;
   for (int p = 0, j = 0; p < s.n; ++p) {
     const uint16_t x = s.start ? s.start[p] : (uint16_t)p;
@@ -564,8 +567,7 @@ __global__ void start_ckpt_kernel(KernelDev d, Chains s) {
     o[0] = st.ptr;
     o[1] = st.fin;
     for (int b = 0; b < 6; ++b) o[2 + b] = st.clr[b];
-    for (int p = j * CK; p < min(s.n, (j + 1) * CK); ++p)
-      st.step(d.meta[s.start ? s.start[p] : p]);
+    for (int p = j * CK; p < min(s.n, (j + 1) * CK); ++p) st.step(tb.meta[s.row0[p]]);
   }
   s.ck0[(size_t)s.nck * 8] = st.total();
 }
@@ -1225,8 +1227,11 @@ static int run_fused(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* se
   }
   size_t sm = smem_need(k->d);
   int use_smem = sm <= kSmemCap;
-  if (use_smem) TRY(configure_smem(ctx, (const void*)anneal_fused_kernel, sm));
-  start_ckpt_kernel<<<1, 32, 0, ctx->stream>>>(k->d, o.s);
+  if (use_smem) {
+    TRY(configure_smem(ctx, (const void*)anneal_fused_kernel, sm));
+    TRY(configure_smem(ctx, (const void*)start_ckpt_kernel, sm));
+  }
+  start_ckpt_kernel<<<1, 128, use_smem ? sm : 0, ctx->stream>>>(k->d, o.s, use_smem);
   anneal_fused_kernel<<<(chains + 127) / 128, 128, use_smem ? sm : 0, ctx->stream>>>(
       k->d, o.s, k->d_base, use_smem, (double)k->baseline);
   cudaError_t e = cudaGetLastError();
