@@ -872,6 +872,7 @@ struct sip_chains {
   int32_t* d_lo = nullptr;
   uint16_t* d_adopt = nullptr;
   uint16_t* d_start = nullptr;
+  sip_chain_summary* d_summary = nullptr;  // packed summaries for one D2H copy
 };
 
 struct sip_results {
@@ -933,7 +934,8 @@ static void chains_free(sip_chains* o) {
   void* ptrs[] = {s.sched, s.best, s.cpos, s.mt, s.mti, s.t0, s.e_x, s.e_best, s.it,
                   s.best_iter, s.ambiguous, s.p_lo, s.p_cand, s.p_dir, s.hist, o->d_temps,
                   o->d_seeds, o->d_tcurr, o->d_status, o->d_lo, s.cand_out, o->d_adopt,
-                  s.ckpt, s.ckpt2, s.ck0, s.row0, s.cpos0, s.acclog, s.replayed, s.priced, o->d_start};
+                  s.ckpt, s.ckpt2, s.ck0, s.row0, s.cpos0, s.acclog, s.replayed, s.priced, o->d_start,
+                  o->d_summary};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -946,6 +948,13 @@ static int fetch_sched(sip_ctx* ctx, const uint16_t* dsrc, int n, int ns, int C,
   return SIP_OK;
 }
 
+__global__ void pack_summary_kernel(Chains s, sip_chain_summary* out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= s.C) return;
+  out[c] = sip_chain_summary{s.t0[c], s.e_best[c], s.e_x[c], s.best_iter[c], s.ambiguous[c],
+                             s.replayed ? s.replayed[c] : 0, s.priced ? s.priced[c] : 0, 0};
+}
+
 static int chains_fetch(sip_chains* o, sip_record* history, uint16_t* best, uint16_t* current,
                         sip_chain_summary* summary) {
   sip_ctx* ctx = o->k->ctx;
@@ -954,21 +963,11 @@ static int chains_fetch(sip_chains* o, sip_record* history, uint16_t* best, uint
   if (history) TRY(d2h(ctx, history, s.hist, C * s.budget));
   if (best) TRY(fetch_sched(ctx, s.best, s.n, s.ns, s.C, best));
   if (current) TRY(fetch_sched(ctx, s.sched, s.n, s.ns, s.C, current));
-  if (summary) {
-    std::vector<double> t0(C), ex(C), eb(C);
-    std::vector<int32_t> bi(C), am(C);
-    std::vector<int64_t> rp(C, 0);
-    std::vector<int32_t> pr(C, 0);
-    if (s.replayed) TRY(d2h(ctx, rp.data(), s.replayed, C));
-    if (s.priced) TRY(d2h(ctx, pr.data(), s.priced, C));
-    TRY(d2h(ctx, t0.data(), s.t0, C));
-    TRY(d2h(ctx, ex.data(), s.e_x, C));
-    TRY(d2h(ctx, eb.data(), s.e_best, C));
-    TRY(d2h(ctx, bi.data(), s.best_iter, C));
-    TRY(d2h(ctx, am.data(), s.ambiguous, C));
-    SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    for (size_t c = 0; c < C; ++c)
-      summary[c] = sip_chain_summary{t0[c], eb[c], ex[c], bi[c], am[c], rp[c], pr[c], 0};
+  if (summary) {  // packed on the device, one copy
+    if (!o->d_summary) TRY(dalloc(ctx, &o->d_summary, C));
+    pack_summary_kernel<<<(int)((C + 255) / 256), 256, 0, ctx->stream>>>(s, o->d_summary);
+    SIP_CHECK_LAUNCH(ctx);
+    TRY(d2h(ctx, summary, o->d_summary, C));
   }
   SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return SIP_OK;
