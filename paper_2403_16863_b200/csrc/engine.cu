@@ -265,7 +265,9 @@ __device__ __forceinline__ void record(const Chains& s, int c, int it, int statu
   r.candidate = (uint16_t)cand;
   r.direction = (uint8_t)dir;
   r.status = (uint8_t)status;
-  if (s.record_hist) s.hist[(size_t)c * s.budget + it] = r;
+  // iteration-major [budget][C]: the fused kernel's lanes record the same iteration
+  // together, so a warp's 32 records are one contiguous 512-byte store
+  if (s.record_hist) s.hist[(size_t)it * s.C + c] = r;
 }
 
 // perturb.sample_action + apply_action checks.  Returns -1 when the move is
@@ -948,6 +950,26 @@ static int fetch_sched(sip_ctx* ctx, const uint16_t* dsrc, int n, int ns, int C,
   return SIP_OK;
 }
 
+// chains [first, first+count) of the iteration-major history, chain-major on the host:
+// one strided 2-D copy (count records per iteration row), then a host transpose
+static int fetch_history(sip_ctx* ctx, const Chains& s, int first, int count, sip_record* out) {
+  if (count <= 0 || s.budget <= 0) return SIP_OK;
+  const size_t rec = sizeof(sip_record);
+  std::vector<sip_record> tmp;
+  sip_record* dst = out;
+  if (count > 1) {
+    tmp.resize((size_t)count * s.budget);
+    dst = tmp.data();
+  }
+  SIP_CUDA(ctx, cudaMemcpy2DAsync(dst, count * rec, s.hist + first, (size_t)s.C * rec, count * rec, s.budget,
+                                  cudaMemcpyDeviceToHost, ctx->stream));
+  SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if (count > 1)  // [budget][count] -> [count][budget]
+    for (int it = 0; it < s.budget; ++it)
+      for (int c = 0; c < count; ++c) out[(size_t)c * s.budget + it] = tmp[(size_t)it * count + c];
+  return SIP_OK;
+}
+
 __global__ void pack_summary_kernel(Chains s, sip_chain_summary* out) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= s.C) return;
@@ -960,7 +982,7 @@ static int chains_fetch(sip_chains* o, sip_record* history, uint16_t* best, uint
   sip_ctx* ctx = o->k->ctx;
   Chains& s = o->s;
   size_t C = s.C;
-  if (history) TRY(d2h(ctx, history, s.hist, C * s.budget));
+  if (history) TRY(fetch_history(ctx, s, 0, (int)C, history));
   if (best) TRY(fetch_sched(ctx, s.best, s.n, s.ns, s.C, best));
   if (current) TRY(fetch_sched(ctx, s.sched, s.n, s.ns, s.C, current));
   if (summary) {  // packed on the device, one copy
@@ -1471,7 +1493,7 @@ int sip_results_fetch(sip_results* r, int32_t first, int32_t count, sip_record* 
   sip_ctx* ctx = r->k->ctx;
   Chains& s = r->ws->s;
   if (count == 0) return SIP_OK;
-  if (history) TRY(d2h(ctx, history, s.hist + (size_t)first * s.budget, (size_t)count * s.budget));
+  if (history) TRY(fetch_history(ctx, s, first, count, history));
   if (best) TRY(fetch_sched(ctx, s.best + (size_t)first * s.ns, s.n, s.ns, count, best));
   if (current) TRY(fetch_sched(ctx, s.sched + (size_t)first * s.ns, s.n, s.ns, count, current));
   SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
