@@ -30,6 +30,8 @@ for rnd in range(rounds):
             lp.block[0] = threads[k]
             lp.grid[0], lp.grid[1] = tgt.S // 256, tgt.B * tgt.H
             lp.smem_bytes = 6 * 128 * 128 * 2 + 1024 + 144 + 4096
+        if os.environ.get("AB_SMEM"):  # variants with deeper rings: give every variant this much
+            lp.smem_bytes = int(os.environ["AB_SMEM"])
         med = ctypes.c_double(); raw = np.zeros(10)
         ctx.check(ctx.lib.sip_measure(m.handle, None, ctypes.byref(lp), 2, 10, 0, ctypes.byref(med),
                                       raw.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
