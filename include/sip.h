@@ -163,6 +163,12 @@ int sip_results_fetch(sip_results* r, int32_t first, int32_t count, sip_record* 
                       uint16_t* best, uint16_t* current);
 int sip_results_destroy(sip_results* r);
 
+/* page-locked host memory for result buffers the device writes whole (chain
+ * summaries): full-rate DMA, no first-touch page faults.  The Python host
+ * recycles these blocks in a pool.                                        */
+int sip_host_alloc(size_t bytes, void** out);
+int sip_host_free(void* p);
+
 /* ---- G2 step mode: external energy (any backend.measure) ------------- */
 int sip_chains_create(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds,
                       const double* t0, int32_t chains, sip_chains** out);

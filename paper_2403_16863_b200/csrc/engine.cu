@@ -1500,6 +1500,25 @@ int sip_results_fetch(sip_results* r, int32_t first, int32_t count, sip_record* 
   return SIP_OK;
 }
 
+int sip_host_alloc(size_t bytes, void** out) {
+  if (!out) return SIP_E_ARG;
+  *out = nullptr;
+  if (cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    *out = nullptr;
+    return SIP_E_CUDA;
+  }
+  return SIP_OK;
+}
+
+int sip_host_free(void* p) {
+  if (p && cudaFreeHost(p) != cudaSuccess) {
+    cudaGetLastError();
+    return SIP_E_CUDA;
+  }
+  return SIP_OK;
+}
+
 int sip_results_destroy(sip_results* r) {
   if (!r) return SIP_OK;
   if (r->ws) {

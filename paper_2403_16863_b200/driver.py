@@ -135,7 +135,9 @@ def run_search(kernel: Kernel, backend, anneal_cfg: AnnealConfig, *, chains: int
                plan=None, store: ResultStore | None = None, on_epoch=None) -> SearchReport:
     if chains < 1:
         raise ValueError("chains must be >= 1")
-    digest = input_hash(serialize_kernel(kernel))
+    digest = kernel.__dict__.get("_input_hash")  # frozen Kernel: hash its text once
+    if digest is None:
+        digest = kernel.__dict__["_input_hash"] = input_hash(serialize_kernel(kernel))
     states = run_states(kernel, backend, anneal_cfg, chains, _tester(kernel, plan, anneal_cfg),
                         on_epoch=on_epoch)
     if plan is None and store is None and hasattr(states, "summ"):

@@ -111,6 +111,8 @@ _SIGS = {
     "sip_results_fetch": ([ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, c_u16p, c_u16p],
                           ctypes.c_int),
     "sip_results_destroy": ([ctypes.c_void_p], ctypes.c_int),
+    "sip_host_alloc": ([ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "sip_host_free": ([ctypes.c_void_p], ctypes.c_int),
     "sip_chains_create": ([ctypes.c_void_p, ctypes.POINTER(AnnealCfg), c_i64p, c_dblp,
                            ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
     "sip_chains_propose": ([ctypes.c_void_p, c_i32p, c_u16p], ctypes.c_int),
@@ -387,7 +389,7 @@ class DeviceKernel:
         seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.int64))
         temps = np.ascontiguousarray(temps, dtype=np.float64)
         C = len(seeds)
-        summ = np.zeros(C, dtype=SUMMARY_DTYPE)
+        summ = pinned_pool(self.ctx.lib).records(C, SUMMARY_DTYPE)
         st = None if start is None else np.ascontiguousarray(start, dtype=np.uint16)
         cfg = self._cfg(temps, unsafe, hw_safe, min_fixed)
         h = ctypes.c_void_p()
@@ -399,6 +401,57 @@ class DeviceKernel:
     def chains(self, seeds, t0, temps: np.ndarray, unsafe: bool = False, hw_safe: bool = False,
                min_fixed: int = 0) -> "StepChains":
         return StepChains(self, seeds, t0, temps, unsafe, hw_safe, min_fixed)
+
+
+class _PinnedPool:
+    """Page-locked host blocks (sip_host_alloc) for results the device writes whole, such
+    as the per-chain summaries: the copy runs at full DMA rate with no first-touch page
+    faults.  A block returns to the pool when the last array viewing it is dropped."""
+
+    def __init__(self, lib):
+        self.lib = lib
+        self.free: dict = {}  # nbytes -> [addresses]
+        self.lock = threading.Lock()
+        self.allocated = 0  # blocks obtained from sip_host_alloc (never returned to CUDA)
+
+    def records(self, count: int, dtype) -> np.ndarray:
+        dtype = np.dtype(dtype)
+        nbytes = max(1, count * dtype.itemsize)
+        with self.lock:
+            blocks = self.free.get(nbytes)
+            addr = blocks.pop() if blocks else None
+        if addr is None:
+            p = ctypes.c_void_p()
+            if self.lib.sip_host_alloc(nbytes, ctypes.byref(p)) != 0 or not p.value:
+                return np.zeros(count, dtype=dtype)  # pageable memory still works
+            addr = p.value
+            self.allocated += 1
+        raw = (ctypes.c_char * nbytes).from_address(addr)
+        raw._block = _PinnedBlock(self, nbytes, addr)  # every view of the array keeps raw alive
+        return np.frombuffer(raw, dtype=np.uint8, count=count * dtype.itemsize).view(dtype)
+
+    def release(self, nbytes: int, addr: int) -> None:
+        with self.lock:
+            self.free.setdefault(nbytes, []).append(addr)
+
+
+_POOL: _PinnedPool | None = None
+
+
+def pinned_pool(lib) -> _PinnedPool:
+    """The process-wide pool (blocks are portable across the per-GPU contexts)."""
+    global _POOL
+    if _POOL is None:
+        _POOL = _PinnedPool(lib)
+    return _POOL
+
+
+class _PinnedBlock:
+    def __init__(self, pool: _PinnedPool, nbytes: int, addr: int):
+        self.pool, self.nbytes, self.addr = pool, nbytes, addr
+
+    def __del__(self):
+        self.pool.release(self.nbytes, self.addr)
 
 
 class DeviceResults:

@@ -168,3 +168,29 @@ def test_anneal_epoch_reduced_matches_oracle_champion():
     assert res["best_seed"] == s and res["champion_chain"] == s - 700
     assert res["best_energy"] == e and np.array_equal(champ, ob)
     assert res["priced"] == priced and res["ambiguous"] == 0
+
+
+def test_pinned_summary_pool_recycles_blocks():
+    """Chain summaries land in page-locked blocks that are reused once every view is gone,
+    and a block stays valid while any view of it is alive."""
+    import gc
+
+    from paper_2403_16863_b200.engine import SUMMARY_DTYPE, pinned_pool
+
+    pool = pinned_pool(get_context().lib)
+    a = pool.records(1000, SUMMARY_DTYPE)
+    addr = a.ctypes.data
+    a["t0"] = 3.5
+    view = a["t0"][10:]
+    del a
+    gc.collect()
+    b = pool.records(1000, SUMMARY_DTYPE)
+    addr_b = b.ctypes.data
+    assert addr_b != addr  # the first block is still held by `view`
+    assert float(view[0]) == 3.5
+    del view, b
+    gc.collect()
+    # both blocks are back in the pool: the next two requests reuse them
+    c = pool.records(1000, SUMMARY_DTYPE)
+    d = pool.records(1000, SUMMARY_DTYPE)
+    assert {c.ctypes.data, d.ctypes.data} == {addr, addr_b}
