@@ -7,7 +7,7 @@ Headline (``value``): candidates evaluated per second by the batched search
 engine.  Workload: the reference's default search (95 iterations, simulator
 energy, AnnealConfig defaults) over the decoded listing of the hand-written
 tcgen05 GEMM+LeakyReLU cubin (the M=N=K=4096 target of configs[1]);
-``--sim-chains`` chains per GPU; one *step* = one epoch: every chain runs its
+``--sim-chains`` chains per GPU (default: two full waves of the fused kernel); one *step* = one epoch: every chain runs its
 95 iterations in one kernel launch, then the ranks all-gather (energy, seed)
 over NCCL and restart from the global champion.  Device time (CUDA events,
 barrier + synchronize on both sides, max over ranks).  ``e2e``: the same
@@ -54,7 +54,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--sim-chains", type=int, default=262144, help="engine chains per GPU")
+    ap.add_argument("--sim-chains", type=int, default=0,
+                    help="engine chains per GPU (0: two full waves of the fused kernel, "
+                         "sip_anneal_wave; 303 104 on a 148-SM B200)")
     ap.add_argument("--chains", type=int, default=16, help="hardware-priced chains per GPU")
     ap.add_argument("--hw-steps", type=int, default=24, help="hardware search rounds")
     ap.add_argument("--classes", default="extended", choices=["global", "extended"],
@@ -501,7 +503,7 @@ def main() -> None:
     dk = ctx.kernel(tables)
     acfg = AnnealConfig()  # reference defaults: T 1.0 -> 0.01, cooling 1.05, 95 iterations
     temps = acfg.temperatures()
-    C = args.sim_chains
+    C = args.sim_chains or 2 * dk.wave_chains()  # whole waves: no partially filled last wave
     best = {"e": 1.0, "perm": None}
 
     def epoch(ep: int):

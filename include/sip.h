@@ -163,6 +163,11 @@ int sip_results_fetch(sip_results* r, int32_t first, int32_t count, sip_record* 
                       uint16_t* best, uint16_t* current);
 int sip_results_destroy(sip_results* r);
 
+/* chains that fill every SM once with the fused simulator-energy kernel (one
+ * chain per thread at its occupancy on this listing): size `chains` of
+ * sip_anneal_epoch / sip_anneal_keep in multiples of it to avoid a partial wave */
+int sip_anneal_wave(sip_kernel* k, int32_t* chains);
+
 /* page-locked host memory for result buffers the device writes whole (chain
  * summaries): full-rate DMA, no first-touch page faults.  The Python host
  * recycles these blocks in a pool.                                        */

@@ -1500,6 +1500,20 @@ int sip_results_fetch(sip_results* r, int32_t first, int32_t count, sip_record* 
   return SIP_OK;
 }
 
+int sip_anneal_wave(sip_kernel* k, int32_t* chains) {
+  if (!k || !chains) return SIP_E_ARG;
+  sip_ctx* ctx = k->ctx;
+  SIP_CUDA(ctx, cudaSetDevice(ctx->device));
+  size_t sm = smem_need(k->d);
+  int use_smem = sm <= kSmemCap;
+  if (use_smem) TRY(configure_smem(ctx, (const void*)anneal_fused_kernel, sm));
+  int per_sm = 0;
+  SIP_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, anneal_fused_kernel, 128,
+                                                              use_smem ? sm : 0));
+  *chains = per_sm * ctx->sm_count * 128;
+  return SIP_OK;
+}
+
 int sip_host_alloc(size_t bytes, void** out) {
   if (!out) return SIP_E_ARG;
   *out = nullptr;

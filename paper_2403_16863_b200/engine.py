@@ -111,6 +111,7 @@ _SIGS = {
     "sip_results_fetch": ([ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, c_u16p, c_u16p],
                           ctypes.c_int),
     "sip_results_destroy": ([ctypes.c_void_p], ctypes.c_int),
+    "sip_anneal_wave": ([ctypes.c_void_p, c_i32p], ctypes.c_int),
     "sip_host_alloc": ([ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
     "sip_host_free": ([ctypes.c_void_p], ctypes.c_int),
     "sip_chains_create": ([ctypes.c_void_p, ctypes.POINTER(AnnealCfg), c_i64p, c_dblp,
@@ -382,6 +383,12 @@ class DeviceKernel:
             None if st is None else _ptr(st, c_u16p), ctypes.byref(res), _ptr(champ, c_u16p)))
         out = {f: getattr(res, f) for f, _ in EpochResult._fields_ if f != "pad"}
         return out, champ
+
+    def wave_chains(self) -> int:
+        """Chains filling every SM once with the fused kernel (sip_anneal_wave)."""
+        v = ctypes.c_int32()
+        self.ctx.check(self.ctx.lib.sip_anneal_wave(self.handle, ctypes.byref(v)))
+        return int(v.value)
 
     def anneal_keep(self, seeds, temps: np.ndarray, start=None, unsafe: bool = False,
                     hw_safe: bool = False, min_fixed: int = 0):
