@@ -167,9 +167,9 @@ def peaks() -> dict:
     return {"tflops": 1590.0, "hbm": 6650.0, "src": "fallback", "tflops_sustained": 1400.0}
 
 
-def ncu_traffic() -> float | None:
-    """dram bytes per launch of the GEMM from the committed ncu --set full summary."""
-    p = ROOT / "profiles" / "gemm_ncu_summary.json"
+def ncu_traffic(kind: str) -> float | None:
+    """dram bytes per launch of a target from its committed ncu --set full summary."""
+    p = ROOT / "profiles" / f"{kind}_ncu_summary.json"
     if p.exists():
         try:
             return float(json.loads(p.read_text())["dram_bytes_per_launch"])
@@ -382,7 +382,7 @@ def hardware_phase(kind, listing, local, rank, world, dist, args, rounds, shape=
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "frac_of_burst_peak": achieved / pk["tflops"],
                 "clocks_during": clocks,
-                "traffic": ncu_traffic() if kind == "gemm" else None,
+                "traffic": ncu_traffic(kind),
                 "kernel": be.listing.func, "flop_per_launch": tgt.flops, "launches_timed": len(kern),
                 "avg_launch_ms": avg_ms,
                 "peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained (power-capped clocks during "

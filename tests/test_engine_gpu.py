@@ -194,3 +194,16 @@ def test_pinned_summary_pool_recycles_blocks():
     c = pool.records(1000, SUMMARY_DTYPE)
     d = pool.records(1000, SUMMARY_DTYPE)
     assert {c.ctypes.data, d.ctypes.data} == {addr, addr_b}
+
+
+def test_anneal_wave_is_whole_blocks_on_every_sm():
+    """sip_anneal_wave: chains of one full wave of the fused kernel (128-thread blocks,
+    at least one resident per SM)."""
+    from bench import decoded_listing
+
+    listing = decoded_listing()
+    dk = get_context().kernel(KernelTables.build(listing.kernel, MachineConfig()))
+    wave = dk.wave_chains()
+    sms = get_context().sm_count
+    assert wave > 0 and wave % (128 * sms) == 0
+    assert wave // (128 * sms) <= 16  # 2 048 threads per SM at most
