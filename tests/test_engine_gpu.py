@@ -7,6 +7,7 @@ import pytest
 
 from conftest import golden, listing_names
 from golden_configs import CONFIGS
+from golden.edge_listings import EDGE_LISTINGS
 from oracle import oracle
 from paper_2403_16863_b200 import (AnnealConfig, SimulatorBackend, anneal, parse_kernel, run_search,
                                    simulate)
@@ -207,3 +208,34 @@ def test_anneal_wave_is_whole_blocks_on_every_sm():
     sms = get_context().sm_count
     assert wave > 0 and wave % (128 * sms) == 0
     assert wave // (128 * sms) <= 16  # 2 048 threads per SM at most
+
+
+# edge-case listings (boundaries, no legal move, cuts, all-candidate, tiny): pinned to
+# the reference by tests/golden/edge.json; the device chains must equal the oracle
+
+
+@pytest.mark.parametrize("name", sorted(EDGE_LISTINGS))
+def test_edge_listings_vs_oracle(name):
+    k = parse_kernel(EDGE_LISTINGS[name], name=name)
+    t = KernelTables.build(k, MachineConfig())
+    dk = get_context().kernel(t)
+    ol = oracle.OracleListing(t)
+    for cname in ("default", "unsafe", "long"):
+        cfg = AnnealConfig(**CONFIGS[cname])
+        temps = cfg.temperatures()
+        seeds = np.arange(64, dtype=np.int64)
+        hist, best, cur, summ = dk.anneal(seeds, temps, unsafe=cfg.unsafe_moves)
+        for c, s in enumerate(seeds):
+            oh, ob, oc, os_ = ol.anneal(int(s), temps, unsafe=cfg.unsafe_moves)
+            assert np.array_equal(hist[c], oh), (name, cname, int(s))
+            assert np.array_equal(best[c], ob) and np.array_equal(cur[c], oc)
+            assert summ["best_energy"][c] == os_["best_energy"]
+
+
+def test_no_candidates_raises_like_the_reference():
+    from paper_2403_16863_b200.perturb import NoCandidatesError
+
+    k = parse_kernel("[B------:R-:W-:-:S04] IADD3 R5, R6, 0x1, RZ ;\n"
+                     "[B------:R-:W-:-:S04] IADD3 R8, R9, 0x1, RZ ;\n", name="alu_only")
+    with pytest.raises(NoCandidatesError):
+        run_search(k, SimulatorBackend(), AnnealConfig(seed=0), chains=4)

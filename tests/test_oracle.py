@@ -69,3 +69,28 @@ def test_oracle_sample_inputs():
         specs = [(5, kinds[rec["kind"]], dists[rec["dist"]]), (3, 4, 0)]
         b0, b1 = oracle.sample_inputs(rec["seed"], rec["index"], specs)
         assert b0.hex() == rec["buf0"] and b1.hex() == rec["buf1"], rec
+
+
+def _edge():
+    import json
+    from pathlib import Path
+
+    return json.loads((Path(__file__).parent / "golden" / "edge.json").read_text())
+
+
+@pytest.mark.parametrize("name", sorted(_edge()))
+def test_oracle_edge_listing_histories(name):
+    """Boundaries, no legal move, cuts, all-candidate and tiny listings: the oracle
+    reproduces the reference's histories (tests/golden/make_edge_golden.py)."""
+    rec = _edge()[name]
+    k = parse_kernel(rec["text"], name=name)
+    ol = oracle.OracleListing(KernelTables.build(k, MachineConfig()))
+    for cname, runs in rec["anneal"].items():
+        cfg_kw = CONFIGS[cname]
+        for seed, want in runs.items():
+            cfg = AnnealConfig(seed=int(seed), **cfg_kw)
+            temps = oracle.temperatures(cfg.t_max, cfg.cooling, cfg.iteration_budget)
+            hist, best, cur, summ = ol.anneal(int(seed), temps, unsafe=cfg.unsafe_moves)
+            jsonl = oracle.history_jsonl(hist, summ["t0"], temps)
+            assert hashlib.sha256(jsonl.encode()).hexdigest() == want["sha256"], (cname, seed)
+            assert best.tolist() == want["best"] and cur.tolist() == want["current"], (cname, seed)
