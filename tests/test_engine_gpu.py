@@ -232,6 +232,28 @@ def test_edge_listings_vs_oracle(name):
             assert summ["best_energy"][c] == os_["best_energy"]
 
 
+def _edge_golden():
+    import json
+    from pathlib import Path
+
+    return json.loads((Path(__file__).parent / "golden" / "edge.json").read_text())
+
+
+@pytest.mark.parametrize("name", sorted(EDGE_LISTINGS))
+def test_edge_listings_public_api_matches_reference(name):
+    """The public anneal() on the edge listings, fused (SimulatorBackend) and step mode
+    (priced through measure()), reproduces the reference's histories and schedules."""
+    want_all = _edge_golden()[name]["anneal"]
+    k = parse_kernel(EDGE_LISTINGS[name], name=name)
+    for cname in ("default", "unsafe", "long"):
+        for seed in (0, 1, 2, 3):
+            want = want_all[cname][str(seed)]
+            for backend in (SimulatorBackend(), _PythonPricedSim()):
+                st = anneal(k, backend, AnnealConfig(seed=seed, **CONFIGS[cname]))
+                assert hashlib.sha256(st.history_jsonl().encode()).hexdigest() == want["sha256"], \
+                    (cname, seed, type(backend).__name__)
+
+
 def test_no_candidates_raises_like_the_reference():
     from paper_2403_16863_b200.perturb import NoCandidatesError
 
