@@ -379,8 +379,14 @@ def hardware_phase(kind, listing, local, rank, world, dist, args, rounds, shape=
     sustained = (clocks.get("sm_mhz") and clocks.get("sm_max_mhz")
                  and clocks["sm_mhz"] < 0.9 * clocks["sm_max_mhz"] and pk.get("tflops_sustained"))
     peak = pk["tflops_sustained"] if sustained else pk["tflops"]
+    # the burst peak scaled to the SM clock this kernel actually ran at (power cap): how
+    # busy the tensor pipe was per cycle, independent of how the cap set the clock
+    scaled = (pk["tflops"] * clocks["sm_mhz"] / clocks["sm_max_mhz"]
+              if clocks.get("sm_mhz") and clocks.get("sm_max_mhz") else None)
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "frac_of_burst_peak": achieved / pk["tflops"],
+                "clock_scaled_peak": scaled,
+                "frac_at_observed_clock": achieved / scaled if scaled else None,
                 "clocks_during": clocks,
                 "traffic": ncu_traffic(kind),
                 "kernel": be.listing.func, "flop_per_launch": tgt.flops, "launches_timed": len(kern),
