@@ -19,6 +19,7 @@
 #include <list>
 #include <string>
 #include <thread>
+#include <unordered_map>
 #include <vector>
 
 #include "common.h"
@@ -119,8 +120,13 @@ struct sip_module {
   int n = 0;
   std::vector<uint8_t> pin;
   std::vector<uint8_t> patched;
-  std::list<CachedMod> cache;  // stable addresses: callers hold CachedMod* across loads
-  size_t cache_cap = 4;        // modules kept loaded (raised for a batch)
+  // loaded schedules in least-recently-used order (front = oldest); std::list keeps
+  // addresses stable (callers hold CachedMod* across loads) and splice is O(1).
+  // `index` maps a hash of the schedule to its entries, so a lookup is O(1) rather than
+  // a scan of every loaded schedule (which made 16 k-candidate rounds lookup-bound).
+  std::list<CachedMod> cache;
+  std::unordered_multimap<uint64_t, std::list<CachedMod>::iterator> index;
+  size_t cache_cap = 4;  // modules kept loaded (raised for a batch)
   uint64_t clock = 0;
   std::vector<cudaEvent_t> events;
 };
@@ -172,12 +178,42 @@ int cu_fail(sip_ctx* ctx, int code, const char* what, CUresult r) {
   return sip::fail(ctx, code, std::string(what) + ": " + (s ? s : "CUDA driver error"));
 }
 
+uint64_t perm_hash(const std::vector<uint16_t>& key) {
+  uint64_t h = 1469598103934665603ull;  // FNV-1a over the 16-bit entries
+  for (uint16_t v : key) h = (h ^ v) * 1099511628211ull;
+  return h ^ key.size();
+}
+
+// the loaded module for schedule `key` (moved to the most-recently-used end), or null
+CachedMod* find_module(sip_module* m, const std::vector<uint16_t>& key) {
+  auto range = m->index.equal_range(perm_hash(key));
+  for (auto it = range.first; it != range.second; ++it)
+    if (it->second->perm == key) {
+      m->cache.splice(m->cache.end(), m->cache, it->second);
+      it->second->stamp = ++m->clock;
+      return &*it->second;
+    }
+  return nullptr;
+}
+
+CachedMod* insert_module(sip_module* m, CachedMod&& cm) {
+  m->cache.push_back(std::move(cm));
+  auto it = std::prev(m->cache.end());
+  m->index.emplace(perm_hash(it->perm), it);
+  return &*it;
+}
+
 // unload the least recently used module that no batch in flight is holding
 void evict_one(sip_module* m) {
-  auto victim = m->cache.end();
-  for (auto it = m->cache.begin(); it != m->cache.end(); ++it)
-    if (!it->pinned && (victim == m->cache.end() || it->stamp < victim->stamp)) victim = it;
+  auto victim = m->cache.begin();
+  while (victim != m->cache.end() && victim->pinned) ++victim;  // pinned entries are recent
   if (victim == m->cache.end()) return;
+  auto range = m->index.equal_range(perm_hash(victim->perm));
+  for (auto it = range.first; it != range.second; ++it)
+    if (it->second == victim) {
+      m->index.erase(it);
+      break;
+    }
   m->ctx->cuModuleUnload(victim->mod);
   m->cache.erase(victim);
 }
@@ -185,12 +221,10 @@ void evict_one(sip_module* m) {
 int get_module(sip_module* m, const uint16_t* perm, CachedMod** out) {
   std::vector<uint16_t> key;
   if (perm) key.assign(perm, perm + m->n);
-  for (auto& c : m->cache)
-    if (c.perm == key) {
-      c.stamp = ++m->clock;
-      *out = &c;
-      return SIP_OK;
-    }
+  if (CachedMod* hit = find_module(m, key)) {
+    *out = hit;
+    return SIP_OK;
+  }
   std::vector<uint8_t> img;
   int rc = build_image(m, perm, img);
   if (rc != SIP_OK) return rc;
@@ -206,8 +240,7 @@ int get_module(sip_module* m, const uint16_t* perm, CachedMod** out) {
   }
   cm.stamp = ++m->clock;
   if (m->cache.size() >= m->cache_cap) evict_one(m);
-  m->cache.push_back(cm);
-  *out = &m->cache.back();
+  *out = insert_module(m, std::move(cm));
   return SIP_OK;
 }
 
@@ -526,12 +559,10 @@ static int measure_batch_impl(sip_module* m, const uint16_t* perm_ref, const uin
   for (int i = 0; i < k; ++i) {
     const uint16_t* p = perms + (size_t)i * m->n;
     std::vector<uint16_t> key(p, p + m->n);
-    for (auto& c : m->cache)
-      if (c.perm == key) {
-        c.stamp = ++m->clock;
-        c.pinned = true;
-        mods[i] = &c;
-      }
+    if (CachedMod* hit = find_module(m, key)) {
+      hit->pinned = true;
+      mods[i] = hit;
+    }
     status[i] = SIP_OK;
     if (!mods[i]) todo.push_back(i);
   }
@@ -576,8 +607,7 @@ static int measure_batch_impl(sip_module* m, const uint16_t* perm_ref, const uin
     cm.stamp = ++m->clock;
     cm.pinned = true;
     if (m->cache.size() >= m->cache_cap) evict_one(m);  // the oldest module not in this batch
-    m->cache.push_back(cm);
-    mods[i] = &m->cache.back();
+    mods[i] = insert_module(m, std::move(cm));
   }
   if (flush_l2 && (rc = ensure_flush(ctx)) != SIP_OK) return rc;
   const int nev = 4 * reps * k;
