@@ -31,11 +31,15 @@ ap.add_argument("--tmax", type=float, default=0.01)
 ap.add_argument("--epoch", type=int, default=10)
 ap.add_argument("--max-seconds", type=float, default=900)
 ap.add_argument("--verify-samples", type=int, default=10_000_000)
+ap.add_argument("--cubin", default=None,
+                help="target cubin file in targets/ (e.g. a build without -lineinfo: same SASS, and "
+                     "the driver's per-load cost then grows far more slowly over a long search)")
 ap.add_argument("--out", required=True)
 a = ap.parse_args()
 
 shape = dict(B=4, H=32, S=4096) if a.target == "attn" else dict(M=4096, N=4096, K=4096)
-tgt = make_target(a.target, **shape).allocate()
+extra = {"cubin_file": a.cubin} if a.cubin else {}
+tgt = make_target(a.target, **shape, **extra).allocate()
 be = B200Backend(tgt)
 ncand = len(candidates(be.kernel, a.classes))
 cfg = AnnealConfig(seed=0, t_max=a.tmax, t_min=a.tmax / 40, cooling=1.02, measure_reps=a.reps,
@@ -59,7 +63,7 @@ ratio, raw = be.ratio(best, 45)
 q1, q3 = np.percentile(raw, [25, 75])
 vr = ver.run(best, a.verify_samples)
 out = {
-    "target": a.target, "shape": shape, "classes": a.classes, "candidates_in_listing": ncand,
+    "target": a.target, "shape": shape, "cubin": a.cubin or "shipped (-lineinfo)", "classes": a.classes, "candidates_in_listing": ncand,
     "listing_instructions": int(be.listing.n), "chains": a.chains, "rounds": rounds,
     "iteration_budget": cfg.iteration_budget, "evaluated": int(hs.evaluated),
     "search_seconds": round(search_s, 1), "candidates_per_s": hs.evaluated / search_s,
