@@ -72,13 +72,6 @@ def build_cubins(force: bool = False) -> dict:
         if force or _stale(cub, deps):
             _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-cubin", "-o", str(cub), str(s)])
         out[name] = cub
-    # the attention target without -lineinfo: byte-identical SASS, for long hardware searches
-    # (the driver's per-load cost grows far faster for cubins with line info)
-    s = TARGETS / CUBINS["attn_fwd"]
-    cub = TARGETS / "attn_nolineinfo.cubin"
-    if s.exists() and (force or _stale(cub, [s] + list(TARGETS.glob("*.cuh")))):
-        _run([NVCC, *ARCH, "-O3", "-std=c++17", "-cubin", "-o", str(cub), str(s)])
-    out["attn_nolineinfo"] = cub
     for name, (src, flags) in CUBIN_VARIANTS.items():
         s = TARGETS / src
         cub = TARGETS / f"{name}.cubin"

@@ -114,7 +114,9 @@ struct CachedMod {
 
 struct sip_module {
   sip_ctx* ctx = nullptr;
-  std::vector<uint8_t> image;
+  std::vector<uint8_t> image;       // the cubin as given (sip_module_patch emits from it)
+  std::vector<uint8_t> load_image;  // the same without debug-section data: what is loaded
+  uint64_t load_text_off = 0;       // .text offset inside load_image
   std::string func;
   uint64_t text_off = 0, text_size = 0;
   int n = 0;
@@ -156,11 +158,107 @@ int neutralize_merc(sip_module* m, std::vector<uint8_t>& img) {
   return SIP_OK;
 }
 
-int build_image(sip_module* m, const uint16_t* perm, std::vector<uint8_t>& out) {
-  out = m->image;
+// Debug sections (-lineinfo: DWARF line tables, SASS/PTX line maps, the embedded PTX text
+// and their .nv.merc copies) do not change the code, but the driver's cuModuleLoadData
+// cost grows with the modules a process has loaded, far faster for images that carry
+// them.  Candidates are loaded from a copy rebuilt without their data:
+// the kept sections' byte ranges are repacked (each keeps its offset modulo 1024, so every
+// alignment holds), section and program headers are remapped, and the debug sections
+// stay in the header table with size 0 so section indices do not change.
+bool is_debug_section(const std::string& name) {
+  static const char* const prefixes[] = {".debug_", ".nv_debug_", ".rela.debug_", ".rela.nv_debug_",
+                                         ".nv.merc.debug_", ".nv.merc.nv_debug_", ".nv.merc.rela.debug_",
+                                         ".nv.merc.rela.nv_debug_"};
+  for (const char* p : prefixes)
+    if (name.rfind(p, 0) == 0) return true;
+  return false;
+}
+
+bool strip_debug(const std::vector<uint8_t>& img, const std::vector<Sec>& secs, std::vector<uint8_t>& out) {
+  Elf64_Ehdr eh;
+  std::memcpy(&eh, img.data(), sizeof eh);
+  if (eh.e_phentsize != sizeof(Elf64_Phdr) && eh.e_phnum) return false;
+  if (eh.e_phoff + (uint64_t)eh.e_phnum * sizeof(Elf64_Phdr) > img.size()) return false;
+  bool any = false;
+  std::vector<std::pair<uint64_t, uint64_t>> ranges;  // kept file data [begin, end)
+  for (const auto& x : secs) {
+    if (is_debug_section(x.name)) {
+      any = true;
+      continue;
+    }
+    if (x.type == SHT_NOBITS || x.type == SHT_NULL || x.size == 0) continue;
+    if (x.off + x.size > img.size()) return false;
+    ranges.push_back({x.off, x.off + x.size});
+  }
+  if (!any) return false;
+  std::sort(ranges.begin(), ranges.end());
+  std::vector<std::pair<uint64_t, uint64_t>> merged;
+  for (auto& r : ranges)
+    if (!merged.empty() && r.first <= merged.back().second)
+      merged.back().second = std::max(merged.back().second, r.second);
+    else
+      merged.push_back(r);
+  std::vector<uint64_t> new_start(merged.size());
+  uint64_t cur = sizeof(Elf64_Ehdr);
+  for (size_t i = 0; i < merged.size(); ++i) {
+    uint64_t want = merged[i].first % 1024;
+    uint64_t base = cur - cur % 1024 + want;
+    if (base < cur) base += 1024;
+    new_start[i] = base;
+    cur = base + (merged[i].second - merged[i].first);
+  }
+  auto map_off = [&](uint64_t off, bool& ok) -> uint64_t {
+    for (size_t i = 0; i < merged.size(); ++i)
+      if (off >= merged[i].first && off <= merged[i].second) return new_start[i] + (off - merged[i].first);
+    ok = false;
+    return 0;
+  };
+  const uint64_t phoff = (cur + 7) & ~7ull;
+  const uint64_t shoff = (phoff + (uint64_t)eh.e_phnum * sizeof(Elf64_Phdr) + 7) & ~7ull;
+  out.assign(shoff + (uint64_t)eh.e_shnum * sizeof(Elf64_Shdr), 0);
+  for (size_t i = 0; i < merged.size(); ++i)
+    std::memcpy(out.data() + new_start[i], img.data() + merged[i].first, merged[i].second - merged[i].first);
+  bool ok = true;
+  for (int i = 0; i < eh.e_phnum; ++i) {
+    Elf64_Phdr ph;
+    std::memcpy(&ph, img.data() + eh.e_phoff + i * sizeof ph, sizeof ph);
+    if (ph.p_offset == eh.e_phoff) {
+      ph.p_offset = phoff;  // the program header table itself (PT_PHDR and its PT_LOAD)
+    } else if (ph.p_filesz > 0 || ph.p_offset != 0) {
+      bool hit = true;
+      const uint64_t o = map_off(ph.p_offset, hit);
+      if (hit) ph.p_offset = o;
+      else if (ph.p_filesz > 0) ok = false;
+    }
+    std::memcpy(out.data() + phoff + i * sizeof ph, &ph, sizeof ph);
+  }
+  for (int i = 0; i < eh.e_shnum; ++i) {
+    Elf64_Shdr sh;
+    std::memcpy(&sh, img.data() + eh.e_shoff + i * sizeof sh, sizeof sh);
+    if (i < (int)secs.size() && is_debug_section(secs[i].name)) {
+      sh.sh_offset = 0;
+      sh.sh_size = 0;
+    } else if (sh.sh_type != SHT_NULL) {
+      bool hit = true;
+      const uint64_t o = map_off(sh.sh_offset, hit);
+      if (hit) sh.sh_offset = o;
+      else if (sh.sh_type != SHT_NOBITS && sh.sh_size > 0) ok = false;
+      else sh.sh_offset = 0;  // an empty section between removed ranges
+    }
+    std::memcpy(out.data() + shoff + i * sizeof sh, &sh, sizeof sh);
+  }
+  eh.e_phoff = eh.e_phnum ? phoff : 0;
+  eh.e_shoff = shoff;
+  std::memcpy(out.data(), &eh, sizeof eh);
+  return ok;
+}
+
+int build_image(sip_module* m, const uint16_t* perm, std::vector<uint8_t>& out, bool for_load = true) {
+  out = for_load ? m->load_image : m->image;
+  const uint64_t toff = for_load ? m->load_text_off : m->text_off;
   if (perm) {
     const uint8_t* src = m->image.data() + m->text_off;
-    uint8_t* dst = out.data() + m->text_off;
+    uint8_t* dst = out.data() + toff;
     std::vector<uint8_t> seen(m->n, 0);
     for (int i = 0; i < m->n; ++i) {
       int p = perm[i];
@@ -357,6 +455,18 @@ int sip_module_open(sip_ctx* ctx, const void* cubin, size_t size, const char* fu
       }
     }
   }
+  m->load_image = m->image;
+  m->load_text_off = m->text_off;
+  std::vector<uint8_t> stripped;
+  if (!getenv("SIP_KEEP_DEBUG") && strip_debug(m->image, secs, stripped)) {
+    std::vector<Sec> s2;
+    std::string e2;
+    if (parse_sections(stripped, s2, e2) && (size_t)tidx < s2.size() && s2[tidx].size == m->text_size &&
+        std::memcmp(stripped.data() + s2[tidx].off, m->image.data() + m->text_off, m->text_size) == 0) {
+      m->load_image.swap(stripped);
+      m->load_text_off = s2[tidx].off;
+    }
+  }
   *out = m;
   return SIP_OK;
 }
@@ -392,7 +502,8 @@ int sip_module_pins(sip_module* m, uint8_t* pin) {
 int sip_module_patch(sip_module* m, const uint16_t* perm, void* out, size_t* size) {
   if (!m || !size) return SIP_E_ARG;
   std::vector<uint8_t> img;
-  int rc = build_image(m, perm, img);
+  // SIP_PATCH_LOAD_IMAGE=1 emits the image the evaluator loads (debug data removed; tests)
+  int rc = build_image(m, perm, img, /*for_load=*/getenv("SIP_PATCH_LOAD_IMAGE") != nullptr);
   if (rc != SIP_OK) return rc;
   if (!out) {
     *size = img.size();

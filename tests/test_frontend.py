@@ -99,3 +99,38 @@ def test_cli_patch_roundtrip(tmp_path):
     assert main(["patch", str(cub), "gemm_lrelu_f16", str(sw), "-o", str(out)]) == 0
     w0, w1 = m0.words(), Module(out.read_bytes(), "gemm_lrelu_f16").words()
     assert (w1[10] == w0[11]).all() and (w1[11] == w0[10]).all() and (w1[12:] == w0[12:]).all()
+
+
+@pytest.mark.parametrize("name,func", [("attn_fwd", "attn_fwd_f16"), ("gemm_lrelu", "gemm_lrelu_f16")])
+def test_load_image_drops_debug_data_keeps_sass(name, func, tmp_path, monkeypatch):
+    """The image the evaluator loads has the -lineinfo debug data removed (the driver's
+    per-load cost grows with it) and byte-identical SASS."""
+    import ctypes
+    import re
+    import shutil
+    import subprocess
+
+    from paper_2403_16863_b200.engine import load_library
+    from paper_2403_16863_b200.targets import TARGET_DIR
+
+    if shutil.which("cuobjdump") is None:
+        pytest.skip("cuobjdump not available")
+    lib = load_library()
+    data = (TARGET_DIR / f"{name}.cubin").read_bytes()
+    m = ctypes.c_void_p()
+    assert lib.sip_module_open(None, data, len(data), func.encode(), ctypes.byref(m)) == 0
+    monkeypatch.setenv("SIP_PATCH_LOAD_IMAGE", "1")
+    size = ctypes.c_size_t()
+    assert lib.sip_module_patch(m, None, None, ctypes.byref(size)) == 0
+    buf = ctypes.create_string_buffer(size.value)
+    assert lib.sip_module_patch(m, None, buf, ctypes.byref(size)) == 0
+    lib.sip_module_close(m)
+    assert size.value < len(data) * 0.5
+    out = tmp_path / "load.cubin"
+    out.write_bytes(buf.raw[: size.value])
+
+    def sass(path):
+        text = subprocess.run(["cuobjdump", "-sass", str(path)], capture_output=True, text=True, check=True).stdout
+        return [ln for ln in text.splitlines() if re.match(r"\s+/\*[0-9a-f]{4}\*/", ln)]
+
+    assert sass(out) == sass(TARGET_DIR / f"{name}.cubin")

@@ -32,8 +32,7 @@ ap.add_argument("--epoch", type=int, default=10)
 ap.add_argument("--max-seconds", type=float, default=900)
 ap.add_argument("--verify-samples", type=int, default=10_000_000)
 ap.add_argument("--cubin", default=None,
-                help="target cubin file in targets/ (e.g. a build without -lineinfo: same SASS, and "
-                     "the driver's per-load cost then grows far more slowly over a long search)")
+                help="attention cubin file in targets/ instead of the shipped one")
 ap.add_argument("--out", required=True)
 a = ap.parse_args()
 
