@@ -296,6 +296,23 @@ def time_flush(device: int, reps: int = 10) -> float:
     return e0.elapsed_time(e1) / reps
 
 
+def warm_launch_ms(be, n: int, reps: int = 10) -> float:
+    """Median device time (ms) of the nvcc schedule launched back to back without an L2
+    flush, as the evaluator's warm-up launches run (not added to the roofline's samples)."""
+    import ctypes
+
+    from paper_2403_16863_b200.engine import c_dblp, c_u16p
+
+    import numpy as np
+
+    ident = np.arange(n, dtype=np.uint16)
+    med = ctypes.c_double()
+    raw = np.zeros(reps, dtype=np.float64)
+    be.ctx.check(be.ctx.lib.sip_measure(be.module.handle, ident.ctypes.data_as(c_u16p), ctypes.byref(be.launch),
+                                        2, reps, 0, ctypes.byref(med), raw.ctypes.data_as(c_dblp)))
+    return med.value
+
+
 def library_tflops(kind, tgt, reps: int = 15) -> dict:
     """Context only: the same operation through the vendor library on the same inputs
     (torch.matmul -> cuBLAS; scaled_dot_product_attention -> cuDNN/flash), median of
@@ -397,19 +414,22 @@ def hardware_phase(kind, listing, local, rank, world, dist, args, rounds, shape=
                 else "fallback 1590 TFLOP/s"}
     # the evaluator's device work per candidate: (warmup + reps) launches of each schedule
     # of the pair, plus the 256 MB L2 flush before every timed launch
+    # the warm-up launches run without a flush before them, i.e. on a warm L2: time them so
     flush_ms = time_flush(local)
+    warm_ms = warm_launch_ms(be, n)
     npair = 2 if be.paired else 1
-    floor_ms = npair * (be.warmup + hcfg.measure_reps) * avg_ms + npair * hcfg.measure_reps * flush_ms
+    floor_ms = (npair * be.warmup * warm_ms
+                + npair * hcfg.measure_reps * (avg_ms + flush_ms))
     hw = {"candidates_per_s": h_eval / (h_ms / 1e3), "rounds": rounds, "chains_per_gpu": args.chains,
           "candidate_classes": args.classes, "candidates_in_listing": int(hs.dk.k),
           "proposals": rounds * args.chains * world, "priced": int(h_eval),
           "evaluator_roofline_candidates_per_s": world * 1e3 / floor_ms,
           "device_busy_frac": (h_eval / (h_ms / 1e3)) / (world * 1e3 / floor_ms),
-          "flush_ms": flush_ms,
+          "flush_ms": flush_ms, "warm_launch_ms": warm_ms,
           "note": "one candidate = re-encode + cuModuleLoadData (8 host threads) + 2 warmup + 5 timed "
                   "(nvcc, candidate) launch pairs, L2 flushed before each timed launch; a round's "
                   "candidates share one CUDA graph; energy = median pair ratio; roofline = device "
-                  "time of those 14 launches + 10 flushes"}
+                  "time of those 14 launches (the 4 warm-up ones on a warm L2) + 10 flushes"}
     res = hs.result()
     if dist:
         hs.exchange()
