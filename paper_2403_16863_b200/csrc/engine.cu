@@ -216,6 +216,13 @@ struct Sb {
     ptr = issue + (int)c_adv(c);
   }
   __device__ __forceinline__ int total() const { return max(fin, ptr); }
+  // every field moved by a constant (the recurrence is built from max and +constant)
+  __device__ __forceinline__ void shift(int o) {
+    ptr += o;
+    fin += o;
+#pragma unroll
+    for (int b = 0; b < 6; ++b) clr[b] += o;
+  }
 };
 
 // ---------------------------------------------------------------------------
@@ -247,8 +254,11 @@ struct Chains {
   uint16_t* cand_out = nullptr;  // [C][n] chain-major candidate schedules (step mode)
   const uint16_t* start = nullptr;  // optional start schedule (identity when null)
   int nck = 0;                      // scoreboard checkpoints per chain (every CK positions)
+  int nck4 = 0;                     // nck rounded up to 4: ckoff row pitch (16-byte aligned rows)
   int32_t* ckpt = nullptr;          // [nck][8][C] state of the current schedule
   int32_t* ckpt2 = nullptr;         // [nck][8][C] state of the candidate being priced
+  int32_t* ckoff = nullptr;         // [C][nck4] constant added to every field of ckpt[j]: an
+                                    // accepted move shifts the later checkpoints lazily here
   int32_t* ck0 = nullptr;           // [nck][8] + total: checkpoints of the start schedule
   uint16_t* row0 = nullptr;         // [ns] the start schedule (zero-padded)
   uint16_t* cpos0 = nullptr;        // [k] candidate positions in the start schedule
@@ -504,8 +514,10 @@ __device__ int ck_price(const uint2* meta, const Chains& s, int c, int lo, int t
   const uint16_t* row = s.sched + (size_t)c * s.ns;
   const int C = s.C, n = s.n;
   int j0 = lo / CK;
+  const int32_t* off = s.ckoff + (size_t)c * s.nck4;
   Sb st;
   ck_get(s.ckpt, s, c, j0, st);
+  st.shift(off[j0]);
   replay_span(meta, row, j0 * CK, lo, st);
   st.step(meta[row[lo + 1]]);
   if ((lo + 1) % CK == 0) ck_put(s.ckpt2, s, c, (lo + 1) / CK, st);
@@ -517,8 +529,9 @@ __device__ int ck_price(const uint2* meta, const Chains& s, int c, int lo, int t
   delta = 0;
   for (p = pb; p < n; p += CK) {
     int j = p / CK;
-    if (ck_shift(s.ckpt, s, c, j, st, delta)) {
+    if (ck_shift(s.ckpt, s, c, j, st, delta)) {  // against the stored state: delta + off[j]
       jconv = j;
+      delta -= off[j];
       return total_x + delta;
     }
     ck_put(s.ckpt2, s, c, j, st);
@@ -533,19 +546,17 @@ __device__ int ck_price(const uint2* meta, const Chains& s, int c, int lo, int t
 // adopt the priced candidate's checkpoints: its own states past lo and before
 // jconv, the current ones shifted by delta from jconv on
 __device__ void ck_commit(const Chains& s, int c, int lo, int jconv, int delta) {
+  int32_t* off = s.ckoff + (size_t)c * s.nck4;
   for (int j = (lo + CK) / CK; j < jconv; ++j) {
     int4* d = ck_at(s.ckpt, s, c, j);
     const int4* x = ck_at(s.ckpt2, s, c, j);
     d[0] = x[0];
     d[1] = x[1];
+    off[j] = 0;
   }
+  // the later checkpoints move by delta: 4 bytes each instead of a 32-byte read-modify-write
   if (delta != 0)
-    for (int j = jconv; j < s.nck; ++j) {
-      int4* d = ck_at(s.ckpt, s, c, j);
-      int4 a = d[0], b = d[1];
-      d[0] = make_int4(a.x + delta, a.y + delta, a.z + delta, a.w + delta);
-      d[1] = make_int4(b.x + delta, b.y + delta, b.z + delta, b.w + delta);
-    }
+    for (int j = jconv; j < s.nck; ++j) off[j] += delta;
 }
 
 // Every chain of a launch starts from the same schedule, so its checkpoints are
@@ -600,6 +611,8 @@ __global__ void __launch_bounds__(128) anneal_fused_kernel(KernelDev d, Chains s
       }
       int4* ck = ck_at(s.ckpt, s, cw + k, 0);
       for (int q = lane; q < nk; q += 32) ck[q] = k0[q];
+      int32_t* off = s.ckoff + (size_t)(cw + k) * s.nck4;
+      for (int q = lane; q < s.nck4; q += 32) off[q] = 0;
     }
     __syncwarp();  // the rows a lane reads below were written by its warp-mates
   }
@@ -912,6 +925,8 @@ static int chains_alloc(sip_ctx* ctx, sip_kernel* k, const sip_anneal_cfg* cfg, 
   s.nck = (s.n + CK - 1) / CK;
   TRY(dalloc(ctx, &s.ckpt, (size_t)s.nck * 8 * C));
   TRY(dalloc(ctx, &s.ckpt2, (size_t)s.nck * 8 * C));
+  s.nck4 = (s.nck + 3) & ~3;
+  TRY(dalloc(ctx, &s.ckoff, (size_t)s.nck4 * C));
   TRY(dalloc(ctx, &s.ck0, (size_t)s.nck * 8 + 4));
   TRY(dalloc(ctx, &s.row0, (size_t)s.ns));
   TRY(dalloc(ctx, &s.cpos0, (size_t)std::max(s.k, 1)));
@@ -936,7 +951,7 @@ static void chains_free(sip_chains* o) {
   void* ptrs[] = {s.sched, s.best, s.cpos, s.mt, s.mti, s.t0, s.e_x, s.e_best, s.it,
                   s.best_iter, s.ambiguous, s.p_lo, s.p_cand, s.p_dir, s.hist, o->d_temps,
                   o->d_seeds, o->d_tcurr, o->d_status, o->d_lo, s.cand_out, o->d_adopt,
-                  s.ckpt, s.ckpt2, s.ck0, s.row0, s.cpos0, s.acclog, s.replayed, s.priced, o->d_start,
+                  s.ckpt, s.ckpt2, s.ckoff, s.ck0, s.row0, s.cpos0, s.acclog, s.replayed, s.priced, o->d_start,
                   o->d_summary};
   for (void* p : ptrs)
     if (p) cudaFree(p);
