@@ -554,9 +554,18 @@ __device__ void ck_commit(const Chains& s, int c, int lo, int jconv, int delta) 
     d[1] = x[1];
     off[j] = 0;
   }
-  // the later checkpoints move by delta: 4 bytes each instead of a 32-byte read-modify-write
-  if (delta != 0)
-    for (int j = jconv; j < s.nck; ++j) off[j] += delta;
+  // the later checkpoints move by delta: 4 bytes each instead of a 32-byte read-modify-write,
+  // 16 bytes per access once aligned (the row pitch nck4 is a multiple of 4; the padding
+  // entries past nck are never read)
+  if (delta != 0) {
+    int j = jconv;
+    for (; j < s.nck && (j & 3); ++j) off[j] += delta;
+    int4* o4 = reinterpret_cast<int4*>(off);
+    for (int q = (j + 3) >> 2; 4 * q < s.nck; ++q) {  // j is aligned here unless it reached nck
+      int4 v = o4[q];
+      o4[q] = make_int4(v.x + delta, v.y + delta, v.z + delta, v.w + delta);
+    }
+  }
 }
 
 // Every chain of a launch starts from the same schedule, so its checkpoints are
