@@ -256,7 +256,6 @@ struct Chains {
   int nck = 0;                      // scoreboard checkpoints per chain (every CK positions)
   int nck4 = 0;                     // nck rounded up to 4: ckoff row pitch (16-byte aligned rows)
   int32_t* ckpt = nullptr;          // [nck][8][C] state of the current schedule
-  int32_t* ckpt2 = nullptr;         // [nck][8][C] state of the candidate being priced
   int32_t* ckoff = nullptr;         // [C][nck4] constant added to every field of ckpt[j]: an
                                     // accepted move shifts the later checkpoints lazily here
   int32_t* ck0 = nullptr;           // [nck][8] + total: checkpoints of the start schedule
@@ -520,7 +519,13 @@ __device__ int ck_price(const uint2* meta, const Chains& s, int c, int lo, int t
   st.shift(off[j0]);
   replay_span(meta, row, j0 * CK, lo, st);
   st.step(meta[row[lo + 1]]);
-  if ((lo + 1) % CK == 0) ck_put(s.ckpt2, s, c, (lo + 1) / CK, st);
+  // the candidate's own states go straight into ckpt (with a zero offset): nearly every
+  // priced move is accepted, and a rejected one restores them (ck_restore)
+  int32_t* offw = s.ckoff + (size_t)c * s.nck4;
+  if ((lo + 1) % CK == 0) {
+    ck_put(s.ckpt, s, c, (lo + 1) / CK, st);
+    offw[(lo + 1) / CK] = 0;
+  }
   st.step(meta[row[lo]]);
   int p = lo + 2;
   int pb = min(n, ((p + CK - 1) / CK) * CK);
@@ -534,7 +539,8 @@ __device__ int ck_price(const uint2* meta, const Chains& s, int c, int lo, int t
       delta -= off[j];
       return total_x + delta;
     }
-    ck_put(s.ckpt2, s, c, j, st);
+    ck_put(s.ckpt, s, c, j, st);  // compared above; only later checkpoints are read again
+    offw[j] = 0;
     int pe = min(n, p + CK);
     replay_span(meta, row, p, pe, st);
     steps += pe - p;
@@ -547,13 +553,7 @@ __device__ int ck_price(const uint2* meta, const Chains& s, int c, int lo, int t
 // jconv, the current ones shifted by delta from jconv on
 __device__ void ck_commit(const Chains& s, int c, int lo, int jconv, int delta) {
   int32_t* off = s.ckoff + (size_t)c * s.nck4;
-  for (int j = (lo + CK) / CK; j < jconv; ++j) {
-    int4* d = ck_at(s.ckpt, s, c, j);
-    const int4* x = ck_at(s.ckpt2, s, c, j);
-    d[0] = x[0];
-    d[1] = x[1];
-    off[j] = 0;
-  }
+  (void)lo;  // checkpoints in (lo, jconv) already hold the candidate's states (ck_price)
   // the later checkpoints move by delta: 4 bytes each instead of a 32-byte read-modify-write,
   // 16 bytes per access once aligned (the row pitch nck4 is a multiple of 4; the padding
   // entries past nck are never read)
@@ -565,6 +565,22 @@ __device__ void ck_commit(const Chains& s, int c, int lo, int jconv, int delta) 
       int4 v = o4[q];
       o4[q] = make_int4(v.x + delta, v.y + delta, v.z + delta, v.w + delta);
     }
+  }
+}
+
+// a rejected candidate: ck_price overwrote checkpoints in (lo / CK, jconv) with its own
+// states; replay the (unchanged) current row from the checkpoint below lo to rebuild them
+__device__ void ck_restore(const uint2* meta, const Chains& s, int c, int lo, int jconv) {
+  const uint16_t* row = s.sched + (size_t)c * s.ns;
+  int32_t* off = s.ckoff + (size_t)c * s.nck4;
+  const int j0 = lo / CK;
+  Sb st;
+  ck_get(s.ckpt, s, c, j0, st);
+  st.shift(off[j0]);
+  for (int j = j0 + 1; j < jconv; ++j) {
+    replay_span(meta, row, (j - 1) * CK, j * CK, st);
+    ck_put(s.ckpt, s, c, j, st);
+    off[j] = 0;
   }
 }
 
@@ -665,6 +681,8 @@ __global__ void __launch_bounds__(128) anneal_fused_kernel(KernelDev d, Chains s
         best_iter = it;
         best_nacc = nacc;  // the best schedule = the current one after nacc accepted swaps
       }
+    } else {
+      ck_restore(tb.meta, s, c, lo, jconv);
     }
     record(s, c, it, acc ? SIP_ST_ACCEPTED : SIP_ST_PRICED, t, lo, cand, dir);
   }
@@ -933,7 +951,6 @@ static int chains_alloc(sip_ctx* ctx, sip_kernel* k, const sip_anneal_cfg* cfg, 
   TRY(dalloc(ctx, &s.hist, (size_t)std::max(s.budget, 1) * C));
   s.nck = (s.n + CK - 1) / CK;
   TRY(dalloc(ctx, &s.ckpt, (size_t)s.nck * 8 * C));
-  TRY(dalloc(ctx, &s.ckpt2, (size_t)s.nck * 8 * C));
   s.nck4 = (s.nck + 3) & ~3;
   TRY(dalloc(ctx, &s.ckoff, (size_t)s.nck4 * C));
   TRY(dalloc(ctx, &s.ck0, (size_t)s.nck * 8 + 4));
@@ -960,7 +977,7 @@ static void chains_free(sip_chains* o) {
   void* ptrs[] = {s.sched, s.best, s.cpos, s.mt, s.mti, s.t0, s.e_x, s.e_best, s.it,
                   s.best_iter, s.ambiguous, s.p_lo, s.p_cand, s.p_dir, s.hist, o->d_temps,
                   o->d_seeds, o->d_tcurr, o->d_status, o->d_lo, s.cand_out, o->d_adopt,
-                  s.ckpt, s.ckpt2, s.ckoff, s.ck0, s.row0, s.cpos0, s.acclog, s.replayed, s.priced, o->d_start,
+                  s.ckpt, s.ckoff, s.ck0, s.row0, s.cpos0, s.acclog, s.replayed, s.priced, o->d_start,
                   o->d_summary};
   for (void* p : ptrs)
     if (p) cudaFree(p);
