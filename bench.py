@@ -186,18 +186,35 @@ def decoded_listing():
     return render_listing((TARGET_DIR / "gemm_lrelu.cubin").read_bytes(), "gemm_lrelu_f16")
 
 
-def cpu_reference_rate(listing, seconds: float, workers: int = 1) -> dict:
-    """Reference search (oracle C port, simulator energy) on the decoded listing."""
-    from oracle import oracle
-    from paper_2403_16863_b200 import AnnealConfig
-    from paper_2403_16863_b200.machine import MachineConfig
-    from paper_2403_16863_b200.tables import KernelTables
+# the reference's default search (anneal.py:28-60): T 1.0 -> 0.01, cooling 1.05 = 95 iterations
+REF_TEMPS = None
 
-    t = KernelTables.build(listing.kernel, MachineConfig())
-    cfg = AnnealConfig()
-    temps = cfg.temperatures()
+
+def ref_temperatures() -> list:
+    """AnnealConfig() defaults restated (anneal.py:47-60), so the CPU arm imports no product code."""
+    global REF_TEMPS
+    if REF_TEMPS is None:
+        import math
+
+        t_max, t_min, cooling = 1.0, 0.01, 1.05
+        budget = math.ceil(math.log(t_max / t_min) / math.log(cooling))
+        from oracle import oracle
+
+        REF_TEMPS = oracle.temperatures(t_max, cooling, budget)
+    return REF_TEMPS
+
+
+def cpu_reference_rate(seconds: float, workers: int = 1, name: str = "gemm_lrelu_f16") -> dict:
+    """Reference search (oracle C port, simulator energy) on the committed decoded listing
+    (tests/golden/listings), with tables packed from the reference's own per-instruction
+    facts (oracle/golden_tables.py): the CPU arm touches no product code."""
+    from oracle import oracle
+    from oracle.golden_tables import load_targets, tables_from_facts
+
+    rec = load_targets()[name]
+    temps = ref_temperatures()
     if workers <= 1:
-        ol = oracle.OracleListing(t)
+        ol = oracle.OracleListing(tables_from_facts(rec))
         t0 = time.perf_counter()
         priced = chains = 0
         while time.perf_counter() - t0 < seconds:
@@ -208,31 +225,26 @@ def cpu_reference_rate(listing, seconds: float, workers: int = 1) -> dict:
     else:
         from concurrent.futures import ProcessPoolExecutor
 
-        per = max(1, int(seconds))
         t0 = time.perf_counter()
         with ProcessPoolExecutor(workers) as ex:
-            futs = [ex.submit(_cpu_worker, listing.text, w, seconds) for w in range(workers)]
+            futs = [ex.submit(_cpu_worker, name, w, seconds) for w in range(workers)]
             res = [f.result() for f in futs]
         dt = time.perf_counter() - t0
         priced = sum(r[0] for r in res)
         chains = sum(r[1] for r in res)
-        del per
     return {"value": priced / dt, "unit": UNIT, "cores": workers, "kind": "port",
             "sample": f"{chains} chains x {len(temps)} iterations of the reference search "
-                      f"(oracle C port, simulator energy) on the decoded gemm_lrelu_f16 listing "
-                      f"(n={listing.n}), {dt:.1f} s"}
+                      f"(oracle C port, simulator energy) on the decoded {name} listing "
+                      f"(n={rec['n']}), {dt:.1f} s"}
 
 
-def _cpu_worker(text, wid, seconds):
+def _cpu_worker(name, wid, seconds):
     sys.path.insert(0, str(ROOT))
     from oracle import oracle
-    from paper_2403_16863_b200 import AnnealConfig, parse_kernel
-    from paper_2403_16863_b200.machine import MachineConfig
-    from paper_2403_16863_b200.tables import KernelTables
+    from oracle.golden_tables import load_targets, tables_from_facts
 
-    k = parse_kernel(text)
-    ol = oracle.OracleListing(KernelTables.build(k, MachineConfig()))
-    temps = AnnealConfig().temperatures()
+    ol = oracle.OracleListing(tables_from_facts(load_targets()[name]))
+    temps = ref_temperatures()
     t0 = time.perf_counter()
     priced = chains = 0
     seed = wid * 1_000_000
@@ -246,15 +258,14 @@ def _cpu_worker(text, wid, seconds):
 def run_reference(args, rank: int) -> None:
     if rank != 0:
         return
-    listing = decoded_listing()
     cores = os.cpu_count() or 1
     per_step = max(1.0, 60.0 / max(1, args.steps + args.warmup))
     for _ in range(args.warmup):
-        cpu_reference_rate(listing, min(per_step, 2.0), workers=cores)
+        cpu_reference_rate(min(per_step, 2.0), workers=cores)
     vals = []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        vals.append(cpu_reference_rate(listing, per_step, workers=cores))
+        vals.append(cpu_reference_rate(per_step, workers=cores))
     wall = time.perf_counter() - t0
     value = sum(v["value"] for v in vals) / len(vals)
     line = {
@@ -272,13 +283,11 @@ def run_reference(args, rank: int) -> None:
 
 
 # ---------------------------------------------------------------------------
-def allreduce(dist, vals, op):
-    import torch
-
-    t = torch.tensor(vals, dtype=torch.float64, device="cuda")
-    if dist:
-        dist.all_reduce(t, op=op)
-    return t.tolist()
+def allreduce(group, vals, op):
+    """Element-wise reduction over ranks (op: parallel.RED_SUM / RED_MAX / RED_MIN)."""
+    if group is None:
+        return [float(v) for v in vals]
+    return group.allreduce(vals, op)
 
 
 def time_flush(device: int, reps: int = 10) -> float:
@@ -356,9 +365,8 @@ def hardware_phase(kind, listing, local, rank, world, dist, args, rounds, shape=
     from paper_2403_16863_b200.targets import make_target
     from paper_2403_16863_b200.verify import Verifier
 
-    MAX = dist.ReduceOp.MAX if dist else None
-    SUM = dist.ReduceOp.SUM if dist else None
-    MIN = dist.ReduceOp.MIN if dist else None
+    from paper_2403_16863_b200.parallel import RED_MAX as MAX, RED_MIN as MIN, RED_SUM as SUM
+
     shape = shape or (SHAPE if kind == "gemm" else ATTN_SHAPE)
     tgt = make_target(kind, device=local, **shape).allocate()
     be = B200Backend(tgt, listing, device=local, warmup=2, flush_l2=True)
@@ -439,9 +447,7 @@ def hardware_phase(kind, listing, local, rank, world, dist, args, rounds, shape=
     ver = Verifier(kind, device=local)
     acc_e, acc_perm, rejected = hs.verified_best(ver)
     if dist:  # every rank screened the same exchanged ranking; rank 0's choice wins
-        bt = torch.from_numpy(acc_perm.astype(np.int32)).cuda()
-        dist.broadcast(bt, 0)
-        acc_perm = bt.cpu().numpy().astype(np.uint16)
+        acc_perm = dist.broadcast_perm(acc_perm, 0)
     tuned = verify = None
     if rank == 0:
         ident = np.arange(n, dtype=np.uint16)
@@ -479,14 +485,33 @@ def hardware_phase(kind, listing, local, rank, world, dist, args, rounds, shape=
     return {"roofline": roofline, "hw": hw, "tuned": tuned, "verify": verify, "launches": h_launch}
 
 
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` without a launcher: start N ranks (one process per GPU) with
+    torch.distributed.run on 127.0.0.1 and pass rank 0's output through."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main() -> None:
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    # test hook: SIP_SHARE_DEVICE=1 runs every rank on cuda:0 (with SIP_DIST_BACKEND=gloo) so
-    # the multi-rank path can be exercised on a one-GPU box; never used for reported numbers
-    if os.environ.get("SIP_SHARE_DEVICE") == "1":
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but the launcher started {world} ranks")
+    # test hook: SIP_SHARE_DEVICE=1 runs every rank on cuda:0 (collectives over gloo: NCCL
+    # refuses two ranks on one device) so the multi-rank path can be exercised on a
+    # one-GPU box; never used for reported numbers
+    share = os.environ.get("SIP_SHARE_DEVICE") == "1"
+    if share:
         local = 0
     if args.impl == "reference":
         run_reference(args, rank)
@@ -496,33 +521,26 @@ def main() -> None:
     import torch
 
     torch.cuda.set_device(local)
+    os.environ["SIP_DEVICE"] = str(local)
+    from paper_2403_16863_b200.engine import get_context
+    from paper_2403_16863_b200.parallel import RED_MAX as MAX, RED_SUM as SUM, NcclGroup, TorchGroup
+
+    ctx = get_context(local)
     dist = None
     if world > 1:
         import torch.distributed as td
 
-        backend = os.environ.get("SIP_DIST_BACKEND", "nccl")
-        if backend == "nccl":
-            td.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            td.init_process_group(backend)
-        dist = td
-    os.environ["SIP_DEVICE"] = str(local)
-    MAX = dist.ReduceOp.MAX if dist else None
-    SUM = dist.ReduceOp.SUM if dist else None
+        # torch.distributed only for the rendezvous (gloo, CPU); the epoch exchange, the
+        # max-over-ranks timings and the verdict merges run over libsip's NCCL communicator
+        td.init_process_group("gloo")
+        dist = TorchGroup(td) if share else NcclGroup(ctx, rank, world, rendezvous=td)
 
     from paper_2403_16863_b200 import AnnealConfig, SimulatorBackend, run_search
-    from paper_2403_16863_b200.engine import get_context
-    from paper_2403_16863_b200.evaluator import B200Backend
-    from paper_2403_16863_b200.hwsearch import HardwareSearch
     from paper_2403_16863_b200.machine import MachineConfig
-    from paper_2403_16863_b200.parallel import exchange_best
     from paper_2403_16863_b200.tables import KernelTables
-    from paper_2403_16863_b200.targets import GemmTarget
-    from paper_2403_16863_b200.verify import Verifier
 
     listing = decoded_listing()
     n = listing.n
-    ctx = get_context(local)
 
     # ================= phase A: batched search engine (headline) =================
     tables = KernelTables.build(listing.kernel, MachineConfig())
@@ -538,8 +556,7 @@ def main() -> None:
         res, champ = dk.anneal_epoch_reduced((ep * world + rank) * C, C, temps, start=best["perm"])
         e_mine = float(res["best_energy"])
         if dist:  # NCCL allgather of (energy, seed, rank); owner broadcasts its champion
-            e_mine, _, _, champ = exchange_best(dist, e_mine, int(res["best_seed"]), champ,
-                                                torch.device("cuda", local))
+            e_mine, _, _, champ = dist.exchange_best(e_mine, int(res["best_seed"]), champ)
         if e_mine < best["e"]:
             best["e"], best["perm"] = e_mine, champ
         return int(res["priced"]), int(res["replayed"]), int(res["ambiguous"])
@@ -582,6 +599,8 @@ def main() -> None:
             rep = run_search(listing.kernel, SimulatorBackend(MachineConfig()),
                              AnnealConfig(seed=(2_000_000 + w * world + rank) * C), chains=C)
             rep.best.state.best_perm
+        if dist:
+            dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -597,10 +616,10 @@ def main() -> None:
         e1.synchronize()
         e_ms = allreduce(dist, [e0.elapsed_time(e1)], MAX)[0]
         e_priced = allreduce(dist, [ep_priced], SUM)[0]
-        tb = sum(a.nbytes for a in (tables.ctrl, tables.lat, tables.klass, tables.reads,
-                                    tables.writes, tables.refs, tables.nrefs, tables.cut, tables.pin))
+        # per step: the seed array and the temperature schedule go down; the listing's tables
+        # are cached on the device per table set (anneal.device_kernel) and are not re-sent
         e2e = {"value": e_priced / (e_ms / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": int(tb + C * 8 + len(temps) * 8),
+               "h2d_bytes_per_step": int(C * 8 + len(temps) * 8),
                "d2h_bytes_per_step": int(C * 48 + len(temps) * 16 + 2 * n * 2),
                "api": "run_search(kernel, SimulatorBackend(), AnnealConfig(seed), chains=C) per step; "
                       "per-chain histories/schedules stay in HBM until accessed (the champion's are "
@@ -613,7 +632,7 @@ def main() -> None:
         attn = hardware_phase("attn", None, local, rank, world, dist, args, rounds=args.attn_steps)
     cpu = None
     if rank == 0 and world == 1:
-        cpu = cpu_reference_rate(listing, args.cpu_seconds, workers=1)
+        cpu = cpu_reference_rate(args.cpu_seconds, workers=1)
     roofline = gemm["roofline"]
     h_launch = gemm["launches"] + (attn["launches"] if attn else 0)
 
@@ -643,7 +662,10 @@ def main() -> None:
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
-        dist.destroy_process_group()
+        dist.close()
+        import torch.distributed as td
+
+        td.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -304,6 +304,40 @@ int sip_target_attn_launch(sip_ctx* ctx, const void* Q, const void* K, const voi
                            int32_t B, int32_t H, int32_t S, int32_t D, float scale,
                            sip_launch* launch, void* params, uint32_t params_cap);
 
+/* ---- multi-GPU epoch exchange (G9) -------------------
+ * One communicator per rank (one process per GPU) over NCCL (NVLink/NVSwitch on
+ * one box).  libnccl.so.2 is opened at run time (the copy the process already
+ * mapped, e.g. torch's, else the system one), so libsip keeps no link-time NCCL
+ * dependency.  The reference runs chains sequentially and ranks them by
+ * (best_time, seed) (driver.py:73-85); chains shard over ranks and every epoch
+ * all ranks adopt the global best under that same key.                       */
+typedef struct sip_comm sip_comm;
+/* one rank's epoch champion: 24 bytes, all-gathered as raw bytes           */
+typedef struct {
+  double energy;   /* best energy of the rank's chains (lower is better)      */
+  int64_t seed;    /* seed of that chain (the ranking tie-break)             */
+  int32_t rank;    /* filled in by sip_nccl_exchange                          */
+  int32_t pad;
+} sip_best;
+#define SIP_RED_SUM 0
+#define SIP_RED_MAX 1
+#define SIP_RED_MIN 2
+/* rank 0 makes the id (ncclGetUniqueId); the caller hands it to the other ranks
+ * (any rendezvous: a TCP store, a file) -- 128 bytes                         */
+int sip_comm_unique_id(uint8_t id[128]);
+int sip_comm_create(sip_ctx* ctx, const uint8_t id[128], int32_t nranks, int32_t rank, sip_comm** out);
+int sip_comm_destroy(sip_comm* comm);
+/* ncclAllGather of every rank's sip_best (24 B each), the winner = min (energy,
+ * seed, rank); then ncclBroadcast of the winner's schedule (n u16) from its owner.
+ * Host buffers: mine/sched_mine in; all (nranks entries, may be NULL), winner and
+ * sched_out (n entries) out.  Collective: every rank calls it each epoch.     */
+int sip_nccl_exchange(sip_comm* comm, const sip_best* mine, const uint16_t* sched_mine, int32_t n,
+                      sip_best* all, sip_best* winner, uint16_t* sched_out);
+/* in-place allreduce of `count` doubles (host buffer), op = SIP_RED_*: the
+ * bench's max-over-ranks device times and summed counters                  */
+int sip_comm_allreduce(sip_comm* comm, double* vals, int32_t count, int32_t op);
+int sip_comm_barrier(sip_comm* comm);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,7 +21,8 @@ LIB = PKG / "libsip.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 
-LIB_SOURCES = ["context.cu", "engine.cu", "evaluator.cu", "verify.cu", "interp.cu", "targets_launch.cu"]
+LIB_SOURCES = ["context.cu", "engine.cu", "evaluator.cu", "verify.cu", "interp.cu", "targets_launch.cu",
+               "comm.cu"]
 CUBINS = {"gemm_lrelu": "gemm_lrelu.cu", "attn_fwd": "attn_fwd.cu", "canary": "canary.cu"}
 # build-time variants for descriptor probes, e.g. {"attn_fwd_vswap": ("attn_fwd.cu", ["-DSIP_VDESC_SWAP"])}
 # (the swapped MN-major LBO/SBO encoding was measured wrong on a B200: max err 0.077 vs 4e-5)

@@ -3,6 +3,7 @@
 // evaluator launches whatever permutation of those cubins the search proposes
 // with exactly these arguments.
 #include <cstring>
+#include <cstdlib>
 
 #include "common.h"
 
@@ -100,7 +101,12 @@ int sip_target_attn_launch(sip_ctx* ctx, const void* Q, const void* K, const voi
   std::memset(launch, 0, sizeof *launch);
   // persistent: one CTA per SM walks the (query-tile pair, head) items
   long items = (long)(S / 256) * B * H;
-  launch->grid[0] = (uint32_t)(items < ctx->sm_count ? items : ctx->sm_count);
+  long ctas = ctx->sm_count;
+  // test hook: fewer persistent CTAs, so a small problem still runs several items per
+  // CTA (carried K/V ring phases, o_free hand-offs) under compute-sanitizer
+  if (const char* cap = std::getenv("SIP_ATTN_MAX_CTAS"))
+    if (std::atol(cap) > 0 && std::atol(cap) < ctas) ctas = std::atol(cap);
+  launch->grid[0] = (uint32_t)(items < ctas ? items : ctas);
   launch->grid[1] = 1;
   launch->grid[2] = 1;
   launch->block[0] = 512;  // TMA + MMA warps, 2 softmax warpgroups, 1 epilogue warpgroup

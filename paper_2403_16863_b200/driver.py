@@ -104,9 +104,14 @@ def _tester(kernel, plan, cfg):
 
 def hardware_config(backend, cfg: AnnealConfig) -> AnnealConfig:
     """Candidates that execute on the GPU must respect stall distances, reuse
-    bits and pinned offsets; the extension is forced on."""
+    bits and pinned offsets; the extension is forced on.
+
+    ``unsafe_moves`` (skip the dependency check, ``perturb.py:86-87``) is forced off:
+    a RAW/WAR swap that runs as real SASS can write stray global memory or leave a
+    sticky fault in the context the engine shares, and hw_safe only checks the
+    neighbours of the swapped pair, not the pair itself."""
     if getattr(backend, "hardware", False):
-        return replace(cfg, hw_safe=True,
+        return replace(cfg, hw_safe=True, unsafe_moves=False,
                        min_fixed_distance=max(cfg.min_fixed_distance, backend.min_fixed))
     return cfg
 

@@ -165,6 +165,14 @@ _SIGS = {
                                 ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                 ctypes.c_int32, ctypes.c_float, ctypes.POINTER(Launch),
                                 ctypes.c_void_p, ctypes.c_uint32], ctypes.c_int),
+    "sip_comm_unique_id": ([c_u8p], ctypes.c_int),
+    "sip_comm_create": ([ctypes.c_void_p, c_u8p, ctypes.c_int32, ctypes.c_int32,
+                         ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "sip_comm_destroy": ([ctypes.c_void_p], ctypes.c_int),
+    "sip_nccl_exchange": ([ctypes.c_void_p, ctypes.c_void_p, c_u16p, ctypes.c_int32, ctypes.c_void_p,
+                           ctypes.c_void_p, c_u16p], ctypes.c_int),
+    "sip_comm_allreduce": ([ctypes.c_void_p, c_dblp, ctypes.c_int32, ctypes.c_int32], ctypes.c_int),
+    "sip_comm_barrier": ([ctypes.c_void_p], ctypes.c_int),
 }
 
 _lib = None

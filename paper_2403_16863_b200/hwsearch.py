@@ -33,9 +33,9 @@ class HardwareSearch:
         self.kernel = backend.kernel
         self.tables = backend.tables_for(self.kernel, self.cfg.candidate_classes)
         self.dk = backend.ctx.kernel(self.tables)
-        self.dist = dist  # torch.distributed module when world_size > 1
-        self.rank = dist.get_rank() if dist else 0
-        self.world = dist.get_world_size() if dist else 1
+        self.dist = dist  # a parallel.NcclGroup / TorchGroup when world_size > 1
+        self.rank = dist.rank if dist else 0
+        self.world = dist.world if dist else 1
         base = cfg.seed if seed0 is None else seed0
         self.seeds = [base + self.rank * chains + c for c in range(chains)]
         self.C = chains
@@ -99,11 +99,7 @@ class HardwareSearch:
         if self.dist is None:
             self.chains.adopt(sched, e, e * self.t0)
             return
-        import torch
-
-        from .parallel import exchange_best
-
-        be, _, _, sched = exchange_best(self.dist, e, seed, sched, torch.device("cuda", self.be.device))
+        be, _, _, sched = self.dist.exchange_best(e, seed, sched)
         self.chains.adopt(sched, be, be * self.t0)
 
     def ranked(self):

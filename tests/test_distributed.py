@@ -7,7 +7,8 @@ import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2403_16863_b200.parallel import exchange_best, merge_verdicts, shard_seeds
+from paper_2403_16863_b200.parallel import (RED_MAX, TorchGroup, exchange_best, merge_verdicts,
+                                            pick_winner, shard_seeds)
 
 
 def _free_port() -> int:
@@ -26,7 +27,13 @@ def _worker(rank, world, port, q):
         e, s, owner, got = exchange_best(dist, energy, 100 + rank, sched)
         # tie on energy: the smaller seed wins (driver.py:81-85 ranking)
         e2, s2, owner2, _ = exchange_best(dist, 0.9, 7 - rank, sched)
-        p, f, ff = merge_verdicts(dist, 1000 + rank, rank, 5000 if rank else -1)
+        g = TorchGroup(dist)
+        p, f, ff = merge_verdicts(g, 1000 + rank, rank, 5000 if rank else -1)
+        # the group interface the bench and HardwareSearch use
+        ge, gs, gowner, ggot = g.exchange_best([0.97, 0.95][rank], 100 + rank, sched)
+        assert (ge, gs, gowner) == (0.95, 101, 1) and ggot.tolist() == list(range(10))[::-1]
+        assert g.allreduce([rank + 1.5], RED_MAX) == [2.5]
+        assert g.broadcast_perm(sched, root=1).tolist() == list(range(10))[::-1]
         seeds = shard_seeds(0, rank, 4, epoch=1, world=world).tolist()
         q.put((rank, e, s, owner, got.tolist(), s2, owner2, p, f, ff, seeds))
     finally:
@@ -50,3 +57,30 @@ def test_exchange_and_merge_two_ranks():
         assert (s2, owner2) == (6, 1)
         assert (p, f, ff) == (2001, 1, 5000)
         assert seeds == [8 + 4 * rank + i for i in range(4)]
+
+
+def test_pick_winner_ranking_key():
+    """driver.py:81-85: best time first, then seed; rank only breaks exact duplicates."""
+    assert pick_winner([(0.9, 5, 0), (0.8, 9, 1)]) == (0.8, 9, 1)
+    assert pick_winner([(0.9, 5, 0), (0.9, 3, 1)]) == (0.9, 3, 1)
+    assert pick_winner([(0.9, 3, 1), (0.9, 3, 0)]) == (0.9, 3, 0)
+
+
+@pytest.mark.gpu
+def test_nccl_group_c_abi_single_rank():
+    """libsip's NCCL communicator (sip_comm_* / sip_nccl_exchange) on one B200: a
+    one-rank group exchanges with itself (the 8-GPU path is the same calls)."""
+    from paper_2403_16863_b200.engine import get_context
+    from paper_2403_16863_b200.parallel import RED_MAX, RED_SUM, NcclGroup
+
+    g = NcclGroup(get_context(0), 0, 1)
+    try:
+        sched = np.arange(1184, dtype=np.uint16)[::-1].copy()
+        e, s, owner, got = g.exchange_best(0.97, 42, sched)
+        assert (e, s, owner) == (0.97, 42, 0) and np.array_equal(got, sched)
+        assert g.allreduce([1.5, -2.0], RED_SUM) == [1.5, -2.0]
+        assert g.allreduce([3.0], RED_MAX) == [3.0]
+        assert np.array_equal(g.broadcast_perm(sched, 0), sched)
+        g.barrier()
+    finally:
+        g.close()

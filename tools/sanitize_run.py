@@ -31,6 +31,16 @@ elif which == "verify":
     from paper_2403_16863_b200.verify import Verifier
     v = Verifier("gemm", batch=4, shape=dict(M=256, N=256, K=256))
     v.run(np.arange(v.module.n, dtype=np.uint16), 8)
+elif which == "attn_multi":
+    # persistent attention with several items per CTA: 16 items on 3 CTAs (5-6 each), so
+    # K/V ring phases, Q reloads and o_free hand-offs carry across items
+    import os
+    os.environ["SIP_ATTN_MAX_CTAS"] = "3"
+    from paper_2403_16863_b200.evaluator import B200Backend
+    from paper_2403_16863_b200.targets import make_target
+    be = B200Backend(make_target("attn", B=1, H=8, S=512).allocate(), paired=False)
+    assert be.launch.grid[0] == 3
+    be.run_perm(None)
 elif which in ("gemm", "attn"):
     from paper_2403_16863_b200.evaluator import B200Backend
     from paper_2403_16863_b200.targets import make_target
