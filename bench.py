@@ -167,6 +167,30 @@ def peaks() -> dict:
     return {"tflops": 1590.0, "hbm": 6650.0, "src": "fallback", "tflops_sustained": 1400.0}
 
 
+def engine_roofline(cand_per_s: float, chains: int, state_bytes: int, sm_mhz) -> dict | None:
+    """Issue and DRAM rooflines of the fused engine kernel.
+
+    The kernel is a serial integer recurrence per chain (no tensor or FP work): its bound is
+    warp-instruction issue, one per scheduler per cycle = 148 SMs x 4 x the SM clock measured
+    during the timed region.  Instructions per priced candidate and DRAM bytes per chain come
+    from the committed ncu capture of the same kernel at the bench's chain count
+    (profiles/engine_ncu_summary.json); the rate is this run's."""
+    p = ROOT / "profiles" / "engine_ncu_summary.json"
+    if not p.exists() or not sm_mhz:
+        return None
+    d = json.loads(p.read_text())
+    inst = d["warp_inst_per_launch"] / d["priced_per_launch"]
+    achieved = inst * cand_per_s
+    peak = 148 * 4 * sm_mhz * 1e6
+    dram_per_chain = (d["dram_read_bytes"] + d["dram_write_bytes"]) / d["chains"]
+    return {"bound": "issue", "achieved": achieved, "peak": peak, "unit": "warp-inst/s",
+            "frac": achieved / peak, "warp_inst_per_candidate": inst,
+            "issue_active_ncu": d.get("issue_active_pct"),
+            "traffic": dram_per_chain * chains, "chain_state_bytes": state_bytes * chains,
+            "traffic_over_state": dram_per_chain / state_bytes,
+            "source": f"profiles/engine_ncu_summary.json ({d.get('source')}); rate and clock from this run"}
+
+
 def ncu_traffic(kind: str) -> float | None:
     """dram bytes per launch of a target from its committed ncu --set full summary."""
     p = ROOT / "profiles" / f"{kind}_ncu_summary.json"
@@ -582,11 +606,15 @@ def main() -> None:
         dist, [priced, replayed, C * len(temps) * args.steps], SUM)
     value = priced_all / (ms_all / 1e3)
     engine = {"kernel": "anneal_fused_kernel", "chains_per_gpu": C, "iterations": len(temps),
+              "history": "recorded for every chain (stays in HBM)",
               "proposals_per_s": props_all / (ms_all / 1e3),
               "scoreboard_steps_per_s": replayed_all / (ms_all / 1e3),
               "avg_replay_steps_per_candidate": replayed_all / max(1.0, priced_all),
               "listing_instructions": n, "candidates_in_listing": int(dk.k),
               "global_best_energy": best["e"], "ambiguous_metropolis": amb}
+
+    engine["roofline"] = engine_roofline(priced_all / world / (ms_all / 1e3), C, dk.state_bytes(len(temps)),
+                                         clk.summary().get("sm_mhz"))
 
     # e2e: the same metric through the public API (Kernel object in, AnnealStates out)
     e2e = None
@@ -649,8 +677,9 @@ def main() -> None:
                                    "the same kernel on the B200",
                        "chains_per_gpu": C, "step": "one epoch = 95 iterations of every chain + "
                                                     "NCCL allgather of (energy, seed) + champion broadcast",
-                       "l2": "engine state < L2 (resident); hardware phase flushes L2 (256 MB) "
-                             "before every timed launch",
+                       "l2": "engine chain state (~10 KB per chain, ~3 GB per GPU) is larger than "
+                             "L2, so every step streams it from HBM; the hardware phase flushes L2 "
+                             "(256 MB) before every timed launch",
                        "parallelism": f"{world} GPU(s), independent chains, allgather per epoch"},
             "roofline": roofline, "engine": engine,
             "hw": gemm["hw"], "tuned": gemm["tuned"], "verify": gemm["verify"],

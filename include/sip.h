@@ -163,6 +163,11 @@ int sip_results_fetch(sip_results* r, int32_t first, int32_t count, sip_record* 
                       uint16_t* best, uint16_t* current);
 int sip_results_destroy(sip_results* r);
 
+/* device bytes one fused chain of `budget` iterations keeps in HBM (its working set:
+ * schedules, MT19937 words, checkpoints, logs, history) -- the denominator of the
+ * engine's DRAM-traffic ratio in bench.py */
+int sip_anneal_state_bytes(sip_kernel* k, int32_t budget, int64_t* per_chain);
+
 /* chains that fill every SM once with the fused simulator-energy kernel (one
  * chain per thread at its occupancy on this listing): size `chains` of
  * sip_anneal_epoch / sip_anneal_keep in multiples of it to avoid a partial wave */
@@ -230,6 +235,16 @@ int sip_measure_paired(sip_module* m, const uint16_t* perm_ref, const uint16_t* 
 /* k candidates (perms: [k][n]) each timed against perm_ref like sip_measure_paired,
  * all from one CUDA graph after parallel cubin loads; per-candidate outputs, and
  * status[i] = SIP_E_MEASURE for a candidate whose cubin failed to load (skipped). */
+/* One nvcc reference per round (backends.py:108-116 median semantics per candidate): the
+ * reference and the k candidates are warmed up once each, then each of `reps` reps launches
+ * all k+1 modules once in a rotated order, event-timed; candidate i's ratio is the median
+ * over reps of t_i / t_ref of the same rep.  Launch slot q uses parameter set L[q % nL]
+ * (nL >= 3 buffer sets larger than L2 in rotation need no flush: flush_l2 = 0).
+ * Replaces backends.ExternalCommandBackend.measure per candidate (backends.py:66-116). */
+int sip_measure_round(sip_module* m, const uint16_t* perm_ref, const uint16_t* perms, int32_t k,
+                      const sip_launch* L, int32_t nL, int32_t warmup, int32_t reps, int32_t flush_l2,
+                      double* ratio_median, double* ref_median_ms, double* cand_median_ms,
+                      double* raw_ratio, int32_t* status);
 int sip_measure_paired_batch(sip_module* m, const uint16_t* perm_ref, const uint16_t* perms, int32_t k,
                              const sip_launch* launch, int32_t warmup, int32_t reps, int32_t flush_l2,
                              double* ratio_median, double* ref_median_ms, double* cand_median_ms,

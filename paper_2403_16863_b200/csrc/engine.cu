@@ -9,8 +9,7 @@
 //   machine.simulate         machine.py:116-161
 // Here a chain is one thread; thousands of chains run per launch.  Legality is
 // O(1) per proposal: one bit of the E matrix built once per listing (G1), so
-// no graph is ever rebuilt.  Per-chain state is stored position-major
-// ([n][chains]) so a warp's 32 chains touch one line per position.
+// no graph is ever rebuilt.  Per-chain state layouts: Chains below.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -228,8 +227,9 @@ struct Sb {
 // ---------------------------------------------------------------------------
 // chain state (device).  Schedules are chain-major rows of `ns` (n rounded up
 // to 8) u16 so a replay streams its own row with 16-byte loads; the MT words,
-// candidate positions and checkpoints are position-major [*, C] (all chains
-// touch the same index in lockstep, so a warp's accesses coalesce).
+// checkpoints, offsets and interval masks are chain-major too (a chain's accesses
+// stay in its own sectors); candidate positions, the accepted-swap log and the
+// history are position-major [*, C] (all chains touch the same index in lockstep).
 struct Chains {
   int C = 0, n = 0, ns = 0, k = 0, budget = 0;
   int record_hist = 1;
@@ -254,14 +254,26 @@ struct Chains {
   uint16_t* cand_out = nullptr;  // [C][n] chain-major candidate schedules (step mode)
   const uint16_t* start = nullptr;  // optional start schedule (identity when null)
   int nck = 0;                      // scoreboard checkpoints per chain (every CK positions)
-  int nck4 = 0;                     // nck rounded up to 4: ckoff row pitch (16-byte aligned rows)
-  int32_t* ckpt = nullptr;          // [nck][8][C] state of the current schedule
-  int32_t* ckoff = nullptr;         // [C][nck4] constant added to every field of ckpt[j]: an
+  int nck4 = 0;                     // nck rounded up to 4: lrw row pitch (16-byte aligned rows)
+  int nck8 = 0, offp = 0;           // ckoff row: fine[nck8] then coarse[ceil(nck/8) rounded to 4]
+  int32_t* ckpt = nullptr;          // [C][nck][8] state of the current schedule (chain-major)
+  int32_t* ckoff = nullptr;         // [C][offp] constant added to every field of ckpt[j]
+                                    // (fine[j] + coarse[j / 8], OffRow below): an
                                     // accepted move shifts the later checkpoints lazily here
-  int32_t* ck0 = nullptr;           // [nck][8] + total: checkpoints of the start schedule
+  int32_t* ck0 = nullptr;           // [nck][8] + total + final ptr: checkpoints of the start schedule
+  uint32_t* lrw = nullptr;          // [C][nck4] per checkpoint interval j: L_j (bits 0-5) = barriers
+                                    // whose first event in the interval is a wait, R_j (8-13) =
+                                    // barriers with any event in it, W_j (16-21) = barriers live at
+                                    // checkpoint j (waited on before being set again, to the end)
+  uint32_t* lrw0 = nullptr;         // [nck4] the same for the start schedule
   uint16_t* row0 = nullptr;         // [ns] the start schedule (zero-padded)
   uint16_t* cpos0 = nullptr;        // [k] candidate positions in the start schedule
   uint16_t* acclog = nullptr;       // [budget][C] lo of every accepted swap (fused kernel)
+  int32_t* nacc = nullptr;          // [C] accepted swaps (fused kernel)
+  int32_t* best_nacc = nullptr;     // [C] the best schedule = the start one after this many of
+                                    // them: fused chains build `best` only when it is read
+                                    // (best_rows_kernel), never during the search
+  int best_lazy = 0;                // 1 for fused chains: best rows are built when fetched
   int64_t* replayed = nullptr;      // [C] scoreboard steps executed (instrumentation)
   int32_t* priced = nullptr;        // [C] priced iterations
 };
@@ -276,13 +288,63 @@ __device__ __forceinline__ void record(const Chains& s, int c, int it, int statu
   r.status = (uint8_t)status;
   // iteration-major [budget][C]: the fused kernel's lanes record the same iteration
   // together, so a warp's 32 records are one contiguous 512-byte store
-  if (s.record_hist) s.hist[(size_t)it * s.C + c] = r;
+  // streaming store: the history is read only when fetched, so it should not evict chain
+  // state from L2
+  if (s.record_hist) {
+    const int4 v = *reinterpret_cast<const int4*>(&r);
+    __stcs(reinterpret_cast<int4*>(s.hist + (size_t)it * s.C + c), v);
+  }
+}
+
+// MT19937 of one fused chain (chain-major row, lazy twist as rng.cuh's mt_next): the
+// operands of the next draw -- words i, i+1 and i+397 mod 624 -- are loaded at the end
+// of the previous one, so a draw never waits on memory.  Valid because draw i writes
+// only word i, which is none of the next draw's operands, and word i+1 read now is the
+// next draw's word i (at i = 623 both are the already regenerated word 0).
+struct ChainMt {
+  uint32_t* st;
+  int mti;          // index of the next draw (always < 624)
+  uint32_t a, b, j;  // its operands
+  __device__ __forceinline__ void load(int i) {
+    a = st[i];
+    b = st[i + 1 < MT_N ? i + 1 : 0];
+    const int k = i + MT_M;
+    j = st[k < MT_N ? k : k - MT_N];
+  }
+  __device__ __forceinline__ uint32_t next() {
+    const int i = mti;
+    const uint32_t y = (a & 0x80000000u) | (b & 0x7fffffffu);
+    uint32_t v = j ^ (y >> 1) ^ ((y & 1u) ? 0x9908b0dfu : 0u);
+    st[i] = v;
+    const int i1 = i + 1 < MT_N ? i + 1 : 0;
+    a = b;
+    b = st[i1 + 1 < MT_N ? i1 + 1 : 0];
+    const int k = i1 + MT_M;
+    j = st[k < MT_N ? k : k - MT_N];
+    mti = i1;
+    v ^= (v >> 11);
+    v ^= (v << 7) & 0x9d2c5680u;
+    v ^= (v << 15) & 0xefc60000u;
+    v ^= (v >> 18);
+    return v;
+  }
+};
+__device__ __forceinline__ uint32_t mt_randbelow(ChainMt& m, uint32_t n) {
+  const int k = 32 - __clz(n);
+  uint32_t r = m.next() >> (32 - k);
+  while (r >= n) r = m.next() >> (32 - k);
+  return r;
+}
+__device__ __forceinline__ double mt_random(ChainMt& m) {
+  const uint32_t a = m.next() >> 5, b = m.next() >> 6;
+  return (a * 67108864.0 + b) * (1.0 / 9007199254740992.0);
 }
 
 // perturb.sample_action + apply_action checks.  Returns -1 when the move is
 // legal (lo/cand/dir filled) or the SIP_ST_* rejection reason.
-__device__ int propose(const KernelDev& d, const uint2* meta, const int16_t* gid, const Chains& s,
-                       int c, MtRef& mt, int& cand, int& dir, int& lo) {
+template <typename Rng>
+__device__ __forceinline__ int propose(const KernelDev& d, const uint2* meta, const int16_t* gid, const Chains& s,
+                                       int c, Rng& mt, int& cand, int& dir, int& lo) {
   uint32_t cell = mt_randbelow(mt, 2u * (uint32_t)s.k);
   cand = (int)(cell >> 1);
   dir = (int)(cell & 1u);  // 0 = UP
@@ -317,10 +379,12 @@ __device__ void copy_best(const Chains& s, int c) {
 }
 
 // Metropolis rule (anneal.py:39-44); counts decisions too close to call.
-__device__ bool metropolis(double delta_e, double temp, MtRef& mt, int& ambiguous) {
+template <typename Rng>
+__device__ __forceinline__ bool metropolis(double delta_e, double temp, Rng& mt, int& ambiguous) {
   if (delta_e < 0) return true;
   double r = mt_random(mt);
-  double p = exp(-delta_e / temp);
+  // exp(-0/T) is exactly 1 (a move that leaves the total unchanged is the common case)
+  double p = delta_e == 0.0 ? 1.0 : exp(-delta_e / temp);
   if (fabs(r - p) <= 4.0 * (nextafter(p, 2.0) - p)) ++ambiguous;
   return r < p;
 }
@@ -331,7 +395,7 @@ struct Staged {
   const int16_t* gid;
 };
 
-__device__ Staged stage_tables(const KernelDev& d, bool use_smem) {
+__device__ __forceinline__ Staged stage_tables(const KernelDev& d, bool use_smem) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   if (!use_smem) return {d.meta, d.gid};
   uint2* m = reinterpret_cast<uint2*>(smem_raw);
@@ -345,58 +409,55 @@ __device__ Staged stage_tables(const KernelDev& d, bool use_smem) {
 }
 
 // init_by_array (CPython's seeding, rng.cuh) for an int seed (<= 2 key words) into one
-// chain-major row of 624 words, eight words per pair of 16-byte accesses: the serial
-// mixing chain stays in registers and every access moves a whole 32-byte sector.
+// chain-major row of 624 words with a single pass of 16-byte stores.  Pass 1 (v_i =
+// (base_i ^ f1(v_{i-1})) + key_j + j, i = 1..623, then i = 1 again) is run twice in
+// registers: once for the value pass 2 starts from (the second v_1), once in lockstep
+// with pass 2 (w_i = (v_i ^ f2(w_{i-1})) - i), so the row is written once and never read
+// back.  Checked word for word against mt_init_by_array by the fused kernel's
+// byte-identical histories.
 __device__ void mt_seed_row(uint32_t* row, const uint32_t* __restrict__ base, const uint32_t* key, int klen) {
-  uint4* r4 = reinterpret_cast<uint4*>(row);
-  // pass 1, i = 1..623: v_i = (base_i ^ f1(v_{i-1})) + key_j + j
-  uint32_t prev = base[0];
+  const auto f1 = [](uint32_t p) { return (p ^ (p >> 30)) * 1664525u; };
+  const auto f2 = [](uint32_t p) { return (p ^ (p >> 30)) * 1566083941u; };
+  // pass 1a: v_1 .. v_623 and the revisit of i = 1 (step 623, key index 623 mod klen)
+  uint32_t prev = __ldg(base);
+  uint32_t v1 = 0;
   int j = 0;
+  for (int i = 1; i < MT_N; ++i) {
+    prev = (__ldg(base + i) ^ f1(prev)) + key[j] + (uint32_t)j;
+    if (i == 1) v1 = prev;
+    if (++j >= klen) j = 0;
+  }
+  const uint32_t v1b = (v1 ^ f1(prev)) + key[j] + (uint32_t)j;  // mt[1] after pass 1
+  // pass 1b (v_i again, from v_1) fused with pass 2 (from the revisited v_1)
+  uint32_t p1 = v1, p2 = v1b;
+  j = klen > 1 ? 1 : 0;  // key index of step i = 2 is 1 mod klen
+  uint4* r4 = reinterpret_cast<uint4*>(row);
   for (int q = 0; q < MT_N / 8; ++q) {
     uint32_t w[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int i = q * 8 + u;
-      if (i == 0) {
-        w[u] = 0u;  // slot 0 is set after the pass (CPython copies word 623 there)
+      if (i < 2) {
+        w[u] = 0u;  // words 0 and 1 are set after the pass
         continue;
       }
-      const uint32_t v = (__ldg(base + i) ^ ((prev ^ (prev >> 30)) * 1664525u)) + key[j] + (uint32_t)j;
-      w[u] = v;
-      prev = v;
+      p1 = (__ldg(base + i) ^ f1(p1)) + key[j] + (uint32_t)j;
       if (++j >= klen) j = 0;
+      p2 = (p1 ^ f2(p2)) - (uint32_t)i;
+      w[u] = p2;
+    }
+    if (q == 0) {
+      // pass 2's last step revisits i = 1 after the wrap (mt[0] = mt[623]) and mt[0] is then
+      // overwritten with 0x80000000: words 0 and 1 are only known at the end
+      reinterpret_cast<uint2*>(row)[1] = make_uint2(w[2], w[3]);
+      r4[1] = make_uint4(w[4], w[5], w[6], w[7]);
+      continue;
     }
     r4[2 * q] = make_uint4(w[0], w[1], w[2], w[3]);
     r4[2 * q + 1] = make_uint4(w[4], w[5], w[6], w[7]);
   }
-  // wrap: mt[0] = mt[623]; the pass's 624th step revisits i = 1
-  row[0] = prev;
-  {
-    const uint32_t v = (row[1] ^ ((prev ^ (prev >> 30)) * 1664525u)) + key[j] + (uint32_t)j;
-    row[1] = v;
-    prev = v;
-  }
-  // pass 2, i = 2..623: v_i = (v'_i ^ f2(v_{i-1})) - i
-  for (int q = 0; q < MT_N / 8; ++q) {
-    const uint4 a = r4[2 * q], b = r4[2 * q + 1];
-    uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int i = q * 8 + u;
-      if (i < 2) continue;
-      const uint32_t v = (w[u] ^ ((prev ^ (prev >> 30)) * 1566083941u)) - (uint32_t)i;
-      w[u] = v;
-      prev = v;
-    }
-    r4[2 * q] = make_uint4(w[0], w[1], w[2], w[3]);
-    r4[2 * q + 1] = make_uint4(w[4], w[5], w[6], w[7]);
-  }
-  // wrap again: mt[0] = mt[623]; the pass's last step is i = 1; then mt[0] = 0x80000000
-  {
-    const uint32_t v = (row[1] ^ ((prev ^ (prev >> 30)) * 1566083941u)) - 1u;
-    row[1] = v;
-  }
-  row[0] = 0x80000000u;
+  const uint32_t w1 = (v1b ^ f2(p2)) - 1u;
+  reinterpret_cast<uint2*>(row)[0] = make_uint2(0x80000000u, w1);
 }
 
 __device__ void chain_init(const KernelDev& d, const int16_t* gid, const Chains& s, int c,
@@ -453,6 +514,36 @@ __device__ __forceinline__ const int4* ck_at(const int32_t* base, const Chains& 
   return reinterpret_cast<const int4*>(base + ((size_t)c * s.nck + j) * 8);
 }
 
+// Lazy checkpoint offsets, two levels: off(j) = fine[j] + coarse[j / 8].  Shifting every
+// checkpoint from j on by d touches the rest of j's aligned block of 8 fine entries (one
+// 32-byte sector) and the coarse entries of the later blocks, instead of every later entry.
+struct OffRow {
+  int32_t* fine;
+  int32_t* coarse;
+  __device__ __forceinline__ OffRow(const Chains& s, int c) {
+    fine = s.ckoff + (size_t)c * s.offp;
+    coarse = fine + s.nck8;
+  }
+  __device__ __forceinline__ int get(int j) const { return fine[j] + coarse[j >> 3]; }
+  __device__ __forceinline__ void zero(int j) const { fine[j] = -coarse[j >> 3]; }
+  __device__ __forceinline__ void shift_from(int j, int d, int nck) const {
+    int4* f4 = reinterpret_cast<int4*>(fine + (j & ~7));
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int base = (j & ~7) + 4 * h;
+      if (base + 3 < j) continue;
+      int4 v = f4[h];
+      if (base >= j) v.x += d;
+      if (base + 1 >= j) v.y += d;
+      if (base + 2 >= j) v.z += d;
+      if (base + 3 >= j) v.w += d;
+      f4[h] = v;
+    }
+    const int ncb = (nck + 7) >> 3;
+    for (int b = (j >> 3) + 1; b < ncb; ++b) coarse[b] += d;
+  }
+};
+
 __device__ __forceinline__ void ck_put(int32_t* base, const Chains& s, int c, int j, const Sb& st) {
   int4* o = ck_at(base, s, c, j);
   o[0] = make_int4(st.ptr, st.fin, st.clr[0], st.clr[1]);
@@ -472,16 +563,26 @@ __device__ __forceinline__ void ck_get(const int32_t* base, const Chains& s, int
   st.clr[5] = b.w;
 }
 
+// Convergence test at checkpoint j (stored state k; the current schedule's actual state is
+// k + o).  Exact, by induction over the (shared) suffix of both schedules:
+//  - only barriers live at j (waited on before being set again, W_j) can ever reach an
+//    issue again; a dead barrier's clock only fed `fin`, compared below;
+//  - if ptr and the live clocks agree up to a shift d, every later issue, completion and
+//    the final ptr move by d.  Then the totals differ by d when the `fin` fields agree up
+//    to d too, or when neither `fin` can exceed the final ptr (pf = the current schedule's,
+//    a lower bound of every later completion maximum): total = max(fin_j, S + d) with
+//    S >= pf the suffix's maximum.
 __device__ __forceinline__ bool ck_shift(const int32_t* base, const Chains& s, int c, int j, const Sb& st,
-                                         int& delta) {
+                                         int o, uint32_t live, int pf, int& delta) {
   Sb k;
   ck_get(base, s, c, j, k);
   const int dl = st.ptr - k.ptr;
-  if (max(st.fin, st.ptr) != max(k.fin, k.ptr) + dl) return false;
 #pragma unroll
   for (int b = 0; b < 6; ++b)
-    if (max(st.clr[b], st.ptr) != max(k.clr[b], k.ptr) + dl) return false;
-  delta = dl;
+    if (((live >> b) & 1u) && max(st.clr[b], st.ptr) != max(k.clr[b], k.ptr) + dl) return false;
+  const int da = dl - o;  // shift against the actual current state
+  if (max(st.fin, st.ptr) != max(k.fin, k.ptr) + dl && !(st.fin <= pf + da && k.fin + o <= pf)) return false;
+  delta = da;
   return true;
 }
 
@@ -508,23 +609,22 @@ __device__ __forceinline__ void replay_span(const uint2* meta, const uint16_t* r
 // total of the current schedule with (lo, lo+1) exchanged; jconv = first
 // checkpoint where the candidate rejoined the current trajectory (nck if never),
 // delta = the constant shift it rejoined with
-__device__ int ck_price(const uint2* meta, const Chains& s, int c, int lo, int total_x, int& jconv,
-                        int& delta, int64_t& steps) {
+__device__ __forceinline__ int ck_price(const uint2* meta, const Chains& s, int c, int lo, int total_x,
+                                        int pf_x, int& jconv, int& delta, int& pf_c, int64_t& steps) {
   const uint16_t* row = s.sched + (size_t)c * s.ns;
   const int C = s.C, n = s.n;
   int j0 = lo / CK;
-  const int32_t* off = s.ckoff + (size_t)c * s.nck4;
+  const OffRow off(s, c);
   Sb st;
   ck_get(s.ckpt, s, c, j0, st);
-  st.shift(off[j0]);
+  st.shift(off.get(j0));
   replay_span(meta, row, j0 * CK, lo, st);
   st.step(meta[row[lo + 1]]);
   // the candidate's own states go straight into ckpt (with a zero offset): nearly every
   // priced move is accepted, and a rejected one restores them (ck_restore)
-  int32_t* offw = s.ckoff + (size_t)c * s.nck4;
   if ((lo + 1) % CK == 0) {
     ck_put(s.ckpt, s, c, (lo + 1) / CK, st);
-    offw[(lo + 1) / CK] = 0;
+    off.zero((lo + 1) / CK);
   }
   st.step(meta[row[lo]]);
   int p = lo + 2;
@@ -532,56 +632,112 @@ __device__ int ck_price(const uint2* meta, const Chains& s, int c, int lo, int t
   replay_span(meta, row, p, pb, st);
   steps += (pb - j0 * CK);
   delta = 0;
+  const uint32_t* lrw = s.lrw + (size_t)c * s.nck4;
   for (p = pb; p < n; p += CK) {
     int j = p / CK;
-    if (ck_shift(s.ckpt, s, c, j, st, delta)) {  // against the stored state: delta + off[j]
+    if (ck_shift(s.ckpt, s, c, j, st, off.get(j), (lrw[j] >> 16) & 63u, pf_x, delta)) {
       jconv = j;
-      delta -= off[j];
+      pf_c = pf_x + delta;
       return total_x + delta;
     }
     ck_put(s.ckpt, s, c, j, st);  // compared above; only later checkpoints are read again
-    offw[j] = 0;
+    off.zero(j);
     int pe = min(n, p + CK);
     replay_span(meta, row, p, pe, st);
     steps += pe - p;
   }
   jconv = s.nck;
+  pf_c = st.ptr;
   return st.total();
+}
+
+// L_j | R_j << 8 of positions [p0, p1) of a row (see Chains::lrw)
+__device__ __forceinline__ uint32_t interval_lr(const uint2* meta, const uint16_t* row, int p0, int p1) {
+  uint32_t L = 0, R = 0;
+  for (int p = p0; p < p1; ++p) {
+    const uint2 m = meta[row[p]];
+    const uint32_t w = m.x & 63u;
+    L |= w & ~R;
+    R |= w | (m.y >> 16);
+  }
+  return L | (R << 8);
+}
+
+// After an accepted swap at (lo, lo+1) the intervals holding the pair need their L/R again
+// and the liveness W_j = L_j | (W_{j+1} & ~R_j) is carried down until it stops changing.
+// Inside one interval R_j cannot change, and L_j only for a barrier both instructions touch
+// and exactly one of them waits on (the first toucher decides whether its first event is
+// a wait); any other swap inside an interval changes nothing.
+__device__ __forceinline__ bool lr_needed(const uint2* meta, const uint16_t* row, int lo) {
+  if (lo / CK != (lo + 1) / CK) return true;  // the pair straddles two intervals
+  const uint2 x = meta[row[lo]], y = meta[row[lo + 1]];
+  const uint32_t common = ((x.x & 63u) | (x.y >> 16)) & ((y.x & 63u) | (y.y >> 16));
+  return (common & (x.x ^ y.x) & 63u) != 0u;
+}
+
+// store the new L/R of the pair's interval(s) and carry W down
+__device__ __forceinline__ void lr_store(const Chains& s, int c, int lo, uint32_t lra, uint32_t lrb) {
+  const int ja = lo / CK, jb = (lo + 1) / CK;
+  uint32_t* lr = s.lrw + (size_t)c * s.nck4;
+  lr[ja] = (lr[ja] & 0x3F0000u) | lra;
+  if (jb != ja) lr[jb] = (lr[jb] & 0x3F0000u) | lrb;
+  uint32_t wnext = jb + 1 < s.nck ? (lr[jb + 1] >> 16) & 63u : 0u;
+  for (int j = jb; j >= 0; --j) {
+    const uint32_t v = lr[j];
+    const uint32_t w = (v & 63u) | (wnext & ~(v >> 8) & 63u);
+    if (j < ja && w == ((v >> 16) & 63u)) break;
+    lr[j] = (v & 0xFFFFu) | (w << 16);
+    wnext = w;
+  }
+}
+
+// L | R << 8 of interval j of `row`, one position per lane (CK == 32): R is the OR of every
+// position's barriers, L the OR of the waits no earlier position touched (exclusive
+// prefix OR by shuffles).  Every lane of the (full) warp takes part.
+__device__ __forceinline__ uint32_t warp_interval_lr(const uint2* meta, const uint16_t* row, int j, int n,
+                                                     int lane) {
+  const int p = j * CK + lane;
+  uint32_t w = 0u, t = 0u;
+  if (p < n) {
+    const uint2 m = meta[row[p]];
+    w = m.x & 63u;
+    t = w | (m.y >> 16);
+  }
+  uint32_t inc = t;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc |= v;
+  }
+  uint32_t excl = __shfl_up_sync(0xffffffffu, inc, 1);
+  if (lane == 0) excl = 0u;
+  const uint32_t L = __reduce_or_sync(0xffffffffu, w & ~excl);
+  const uint32_t R = __shfl_sync(0xffffffffu, inc, 31);
+  return L | (R << 8);
 }
 
 // adopt the priced candidate's checkpoints: its own states past lo and before
 // jconv, the current ones shifted by delta from jconv on
-__device__ void ck_commit(const Chains& s, int c, int lo, int jconv, int delta) {
-  int32_t* off = s.ckoff + (size_t)c * s.nck4;
+__device__ __forceinline__ void ck_commit(const Chains& s, int c, int lo, int jconv, int delta) {
   (void)lo;  // checkpoints in (lo, jconv) already hold the candidate's states (ck_price)
-  // the later checkpoints move by delta: 4 bytes each instead of a 32-byte read-modify-write,
-  // 16 bytes per access once aligned (the row pitch nck4 is a multiple of 4; the padding
-  // entries past nck are never read)
-  if (delta != 0) {
-    int j = jconv;
-    for (; j < s.nck && (j & 3); ++j) off[j] += delta;
-    int4* o4 = reinterpret_cast<int4*>(off);
-    for (int q = (j + 3) >> 2; 4 * q < s.nck; ++q) {  // j is aligned here unless it reached nck
-      int4 v = o4[q];
-      o4[q] = make_int4(v.x + delta, v.y + delta, v.z + delta, v.w + delta);
-    }
-  }
+  if (delta != 0 && jconv < s.nck) OffRow(s, c).shift_from(jconv, delta, s.nck);
 }
 
 // a rejected candidate: ck_price overwrote checkpoints in (lo / CK, jconv) with its own
 // states; replay the (unchanged) current row from the checkpoint below lo to rebuild them
-__device__ void ck_restore(const uint2* meta, const Chains& s, int c, int lo, int jconv) {
+__device__ __forceinline__ int ck_restore(const uint2* meta, const Chains& s, int c, int lo, int jconv) {
   const uint16_t* row = s.sched + (size_t)c * s.ns;
-  int32_t* off = s.ckoff + (size_t)c * s.nck4;
+  const OffRow off(s, c);
   const int j0 = lo / CK;
   Sb st;
   ck_get(s.ckpt, s, c, j0, st);
-  st.shift(off[j0]);
+  st.shift(off.get(j0));
   for (int j = j0 + 1; j < jconv; ++j) {
     replay_span(meta, row, (j - 1) * CK, j * CK, st);
     ck_put(s.ckpt, s, c, j, st);
-    off[j] = 0;
+    off.zero(j);
   }
+  return jconv > j0 + 1 ? (jconv - 1 - j0) * CK : 0;  // scoreboard steps replayed
 }
 
 // Every chain of a launch starts from the same schedule, so its checkpoints are
@@ -608,14 +764,27 @@ __global__ void start_ckpt_kernel(KernelDev d, Chains s, int use_smem) {
     for (int p = j * CK; p < min(s.n, (j + 1) * CK); ++p) st.step(tb.meta[s.row0[p]]);
   }
   s.ck0[(size_t)s.nck * 8] = st.total();
+  s.ck0[(size_t)s.nck * 8 + 1] = st.ptr;
+  uint32_t wnext = 0;
+  for (int j = s.nck - 1; j >= 0; --j) {
+    const uint32_t v = interval_lr(tb.meta, s.row0, j * CK, min(s.n, (j + 1) * CK));
+    wnext = (v & 63u) | (wnext & ~(v >> 8) & 63u);
+    s.lrw0[j] = v | (wnext << 16);
+  }
+  for (int j = s.nck; j < s.nck4; ++j) s.lrw0[j] = 0;
 }
 
 
 // ---- fused simulator-energy annealing: whole chain in one launch ----------
-__global__ void __launch_bounds__(128) anneal_fused_kernel(KernelDev d, Chains s,
-                                                           const uint32_t* mt_base, int use_smem,
-                                                           double t0_cycles) {
-  Staged tb = stage_tables(d, use_smem);
+// SMEM is a template parameter so the staged tables are addressed as shared memory
+// (LDS) rather than through generic loads chosen at run time
+#ifndef SIP_MINB
+#define SIP_MINB 6  // 6 resident 128-thread blocks per SM (<= 80 registers): measured best of 4-8
+#endif
+template <bool SMEM>
+__global__ void __launch_bounds__(128, SIP_MINB) anneal_fused_kernel(KernelDev d, Chains s,
+                                                           const uint32_t* mt_base, double t0_cycles) {
+  Staged tb = stage_tables(d, SMEM);
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   {
     // every chain starts from the same schedule: the warp writes its 32 chains' rows and
@@ -628,51 +797,61 @@ __global__ void __launch_bounds__(128) anneal_fused_kernel(KernelDev d, Chains s
     const int nq = s.ns / 8, nk = 2 * s.nck;
     for (int k = 0; k < 32 && cw + k < s.C; ++k) {
       uint4* sr = reinterpret_cast<uint4*>(s.sched + (size_t)(cw + k) * s.ns);
-      uint4* br = reinterpret_cast<uint4*>(s.best + (size_t)(cw + k) * s.ns);
-      for (int q = lane; q < nq; q += 32) {
-        const uint4 v = r0[q];
-        sr[q] = v;
-        br[q] = v;
-      }
+      for (int q = lane; q < nq; q += 32) sr[q] = r0[q];
       int4* ck = ck_at(s.ckpt, s, cw + k, 0);
       for (int q = lane; q < nk; q += 32) ck[q] = k0[q];
-      int32_t* off = s.ckoff + (size_t)(cw + k) * s.nck4;
-      for (int q = lane; q < s.nck4; q += 32) off[q] = 0;
+      int32_t* off = s.ckoff + (size_t)(cw + k) * s.offp;
+      for (int q = lane; q < s.offp; q += 32) off[q] = 0;
+      uint32_t* lr = s.lrw + (size_t)(cw + k) * s.nck4;
+      for (int q = lane; q < s.nck4; q += 32) lr[q] = s.lrw0[q];
     }
     __syncwarp();  // the rows a lane reads below were written by its warp-mates
   }
+  // a full warp recomputes interval masks cooperatively (warp_interval_lr)
+  const bool full_warp = CK == 32 && __ballot_sync(0xffffffffu, c < s.C) == 0xffffffffu;
+  const int lane = threadIdx.x & 31;
   if (c >= s.C) return;
   for (int j = 0; j < s.k; ++j) s.cpos[(size_t)j * s.C + c] = s.cpos0[j];
-  MtRef mt{s.mt + (size_t)c * MT_N, 1, MT_N};  // chain-major: a chain's draws stay in its own sectors
+  ChainMt mt;  // chain-major row: a chain's draws stay in its own sectors
+  mt.st = s.mt + (size_t)c * MT_N;
   {
     uint32_t key[2];
     const int klen = mt_key_from_int(s.seeds[c], key);
     mt_seed_row(mt.st, mt_base, key, klen);
-    mt.mti = MT_N;
+    mt.mti = 0;  // seeding leaves mti = 624: the first draw starts a round at word 0
+    mt.load(0);
   }
   const double t0 = t0_cycles;
   int total_x = s.ck0[(size_t)s.nck * 8];
+  int pf_x = s.ck0[(size_t)s.nck * 8 + 1];  // the current schedule's final issue pointer
   int64_t steps = 0;  // scoreboard steps replayed by this chain (the start replay is shared)
   double e_x = (double)total_x / t0, e_best = e_x;
   int best_iter = -1, amb = 0, priced = 0, nacc = 0, best_nacc = 0;
   for (int it = 0; it < s.budget; ++it) {
     int cand, dir, lo;
     int st = propose(d, tb.meta, tb.gid, s, c, mt, cand, dir, lo);
-    if (st >= 0) {
-      record(s, c, it, st, 0.0, lo, cand, dir);
-      continue;
-    }
+    double t = 0.0;
+    bool lr_need = false;
+    if (st < 0) {
     ++priced;
-    int jconv, delta;
-    int tc = ck_price(tb.meta, s, c, lo, total_x, jconv, delta, steps);
-    double t = (double)tc;
+    int jconv, delta, pf_c;
+    int tc = ck_price(tb.meta, s, c, lo, total_x, pf_x, jconv, delta, pf_c, steps);
+    t = (double)tc;
     double e_c = t / t0;
     double de = e_c - e_x;
     bool acc = metropolis(de, s.temps[it], mt, amb);
     if (acc) {
       apply_swap(tb.gid, s, c, lo, cand, dir);
       ck_commit(s, c, lo, jconv, delta);
-      s.acclog[(size_t)nacc * s.C + c] = (uint16_t)lo;
+      lr_need = lr_needed(tb.meta, s.sched + (size_t)c * s.ns, lo);
+      if (lr_need && !full_warp) {
+        const uint16_t* row = s.sched + (size_t)c * s.ns;
+        const int ja = lo / CK, jb = (lo + 1) / CK;
+        lr_store(s, c, lo, interval_lr(tb.meta, row, ja * CK, min(s.n, (ja + 1) * CK)),
+                 interval_lr(tb.meta, row, jb * CK, min(s.n, (jb + 1) * CK)));
+      }
+      pf_x = pf_c;
+      __stcs(s.acclog + (size_t)nacc * s.C + c, (unsigned short)lo);
       ++nacc;
       total_x = tc;
       e_x = e_c;
@@ -682,30 +861,63 @@ __global__ void __launch_bounds__(128) anneal_fused_kernel(KernelDev d, Chains s
         best_nacc = nacc;  // the best schedule = the current one after nacc accepted swaps
       }
     } else {
-      ck_restore(tb.meta, s, c, lo, jconv);
+      steps += ck_restore(tb.meta, s, c, lo, jconv);
     }
-    record(s, c, it, acc ? SIP_ST_ACCEPTED : SIP_ST_PRICED, t, lo, cand, dir);
-  }
-  if (best_iter >= 0) {
-    // best row = current row with the swaps accepted after the best undone (adjacent
-    // swaps are their own inverse), instead of a full row copy at every new best
-    copy_best(s, c);
-    uint16_t* b = s.best + (size_t)c * s.ns;
-    for (int q = nacc - 1; q >= best_nacc; --q) {
-      const int l = s.acclog[(size_t)q * s.C + c];
-      const uint16_t t = b[l];
-      b[l] = b[l + 1];
-      b[l + 1] = t;
+    st = acc ? SIP_ST_ACCEPTED : SIP_ST_PRICED;
     }
+    if (full_warp) {
+      // the warp recomputes each accepting lane's interval masks together (the swap a lane
+      // just wrote is visible to its warp-mates after __syncwarp)
+      __syncwarp();
+      uint32_t todo = __ballot_sync(0xffffffffu, lr_need);
+      uint32_t lra = 0u, lrb = 0u;
+      while (todo) {
+        const int L = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const int loL = __shfl_sync(0xffffffffu, lo, L);
+        const uint16_t* rowL = s.sched + (size_t)(c - lane + L) * s.ns;
+        const uint32_t va = warp_interval_lr(tb.meta, rowL, loL / CK, s.n, lane);
+        const uint32_t vb = (loL + 1) / CK != loL / CK ? warp_interval_lr(tb.meta, rowL, (loL + 1) / CK, s.n, lane) : 0u;
+        if (lane == L) {
+          lra = va;
+          lrb = vb;
+        }
+      }
+      if (lr_need) lr_store(s, c, lo, lra, lrb);
+    }
+    record(s, c, it, st, t, lo, cand, dir);  // one (streaming) store point per iteration
   }
+  s.nacc[c] = nacc;
+  s.best_nacc[c] = best_iter >= 0 ? best_nacc : 0;  // no new best: the start schedule
   s.t0[c] = t0;
   s.e_x[c] = e_x;
   s.e_best[c] = e_best;
   s.best_iter[c] = best_iter;
   s.ambiguous[c] = amb;
-  s.mti[c] = mt.mti;
+  s.mti[c] = mt.mti == 0 ? MT_N : mt.mti;  // 624: the next draw starts a round (rng.cuh)
   s.replayed[c] = steps;
   s.priced[c] = priced;
+}
+
+// best rows of fused chains [first, first + count): the current row with the swaps accepted
+// after the best one undone (adjacent swaps are their own inverse).  One warp per chain: the
+// row copy is coalesced, then one lane replays the short undo log.
+__global__ void best_rows_kernel(Chains s, int first, int count) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= count) return;
+  const int c = first + w;
+  const uint4* src = reinterpret_cast<const uint4*>(s.sched + (size_t)c * s.ns);
+  uint4* dst = reinterpret_cast<uint4*>(s.best + (size_t)c * s.ns);
+  for (int q = lane; q < s.ns / 8; q += 32) dst[q] = src[q];
+  __syncwarp();
+  if (lane != 0) return;
+  uint16_t* b = s.best + (size_t)c * s.ns;
+  for (int q = s.nacc[c] - 1; q >= s.best_nacc[c]; --q) {
+    const int l = s.acclog[(size_t)q * s.C + c];
+    const uint16_t t = b[l];
+    b[l] = b[l + 1];
+    b[l + 1] = t;
+  }
 }
 
 // ---- step mode: externally priced candidates -------------------------------
@@ -952,11 +1164,17 @@ static int chains_alloc(sip_ctx* ctx, sip_kernel* k, const sip_anneal_cfg* cfg, 
   s.nck = (s.n + CK - 1) / CK;
   TRY(dalloc(ctx, &s.ckpt, (size_t)s.nck * 8 * C));
   s.nck4 = (s.nck + 3) & ~3;
-  TRY(dalloc(ctx, &s.ckoff, (size_t)s.nck4 * C));
+  s.nck8 = (s.nck + 7) & ~7;
+  s.offp = s.nck8 + ((((s.nck + 7) >> 3) + 3) & ~3);
+  TRY(dalloc(ctx, &s.ckoff, (size_t)s.offp * C));
   TRY(dalloc(ctx, &s.ck0, (size_t)s.nck * 8 + 4));
+  TRY(dalloc(ctx, &s.lrw, (size_t)s.nck4 * C));
+  TRY(dalloc(ctx, &s.lrw0, (size_t)s.nck4));
   TRY(dalloc(ctx, &s.row0, (size_t)s.ns));
   TRY(dalloc(ctx, &s.cpos0, (size_t)std::max(s.k, 1)));
   TRY(dalloc(ctx, &s.acclog, (size_t)std::max(s.budget, 1) * C));
+  TRY(dalloc(ctx, &s.nacc, C));
+  TRY(dalloc(ctx, &s.best_nacc, C));
   TRY(dalloc(ctx, &s.replayed, C));
   TRY(dalloc(ctx, &s.priced, C));
   SIP_CUDA(ctx, cudaMemsetAsync(s.replayed, 0, sizeof(int64_t) * C, ctx->stream));
@@ -977,7 +1195,7 @@ static void chains_free(sip_chains* o) {
   void* ptrs[] = {s.sched, s.best, s.cpos, s.mt, s.mti, s.t0, s.e_x, s.e_best, s.it,
                   s.best_iter, s.ambiguous, s.p_lo, s.p_cand, s.p_dir, s.hist, o->d_temps,
                   o->d_seeds, o->d_tcurr, o->d_status, o->d_lo, s.cand_out, o->d_adopt,
-                  s.ckpt, s.ckoff, s.ck0, s.row0, s.cpos0, s.acclog, s.replayed, s.priced, o->d_start,
+                  s.ckpt, s.ckoff, s.ck0, s.lrw, s.lrw0, s.row0, s.cpos0, s.acclog, s.nacc, s.best_nacc, s.replayed, s.priced, o->d_start,
                   o->d_summary};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -1018,12 +1236,21 @@ __global__ void pack_summary_kernel(Chains s, sip_chain_summary* out) {
                              s.replayed ? s.replayed[c] : 0, s.priced ? s.priced[c] : 0, 0};
 }
 
+// fused chains keep no best rows during the search: build those of [first, first + count)
+static int ensure_best(sip_ctx* ctx, const Chains& s, int first, int count) {
+  if (!s.best_lazy || count <= 0) return SIP_OK;
+  best_rows_kernel<<<(count + 3) / 4, 128, 0, ctx->stream>>>(s, first, count);
+  SIP_CHECK_LAUNCH(ctx);
+  return SIP_OK;
+}
+
 static int chains_fetch(sip_chains* o, sip_record* history, uint16_t* best, uint16_t* current,
                         sip_chain_summary* summary) {
   sip_ctx* ctx = o->k->ctx;
   Chains& s = o->s;
   size_t C = s.C;
   if (history) TRY(fetch_history(ctx, s, 0, (int)C, history));
+  if (best) TRY(ensure_best(ctx, s, 0, s.C));
   if (best) TRY(fetch_sched(ctx, s.best, s.n, s.ns, s.C, best));
   if (current) TRY(fetch_sched(ctx, s.sched, s.n, s.ns, s.C, current));
   if (summary) {  // packed on the device, one copy
@@ -1281,6 +1508,7 @@ static int run_fused(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* se
     TRY(h2d(ctx, k->d_base, mt_base_host().data(), MT_N));
   }
   o.s.record_hist = record_hist ? 1 : 0;
+  o.s.best_lazy = 1;
   o.s.start = nullptr;
   if (start) {
     if (!o.d_start) TRY(dalloc(ctx, &o.d_start, (size_t)o.s.n));
@@ -1290,12 +1518,16 @@ static int run_fused(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* se
   size_t sm = smem_need(k->d);
   int use_smem = sm <= kSmemCap;
   if (use_smem) {
-    TRY(configure_smem(ctx, (const void*)anneal_fused_kernel, sm));
+    TRY(configure_smem(ctx, (const void*)anneal_fused_kernel<true>, sm));
     TRY(configure_smem(ctx, (const void*)start_ckpt_kernel, sm));
   }
   start_ckpt_kernel<<<1, 128, use_smem ? sm : 0, ctx->stream>>>(k->d, o.s, use_smem);
-  anneal_fused_kernel<<<(chains + 127) / 128, 128, use_smem ? sm : 0, ctx->stream>>>(
-      k->d, o.s, k->d_base, use_smem, (double)k->baseline);
+  if (use_smem)
+    anneal_fused_kernel<true><<<(chains + 127) / 128, 128, sm, ctx->stream>>>(k->d, o.s, k->d_base,
+                                                                             (double)k->baseline);
+  else
+    anneal_fused_kernel<false><<<(chains + 127) / 128, 128, 0, ctx->stream>>>(k->d, o.s, k->d_base,
+                                                                              (double)k->baseline);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ctx, SIP_E_CUDA, std::string("anneal: ") + cudaGetErrorString(e));
   return SIP_OK;
@@ -1323,6 +1555,7 @@ int sip_anneal_ex(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds
       if (sum[c].best_energy < sum[w].best_energy ||
           (sum[c].best_energy == sum[w].best_energy && seeds[c] < seeds[w]))
         w = c;
+    TRY(ensure_best(ctx, o.s, w, 1));
     SIP_CUDA(ctx, cudaMemcpyAsync(champion, o.s.best + (size_t)w * o.s.ns, sizeof(uint16_t) * o.s.n,
                                   cudaMemcpyDeviceToHost, ctx->stream));
     SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
@@ -1393,7 +1626,9 @@ extern "C" {
 int sip_anneal_epoch(sip_kernel* k, const sip_anneal_cfg* cfg, int64_t seed_base, int32_t chains,
                      const uint16_t* start, sip_epoch_result* result, uint16_t* champion) {
   if (!k || !cfg || !result || !champion) return SIP_E_ARG;
-  int rc = run_fused(k, cfg, nullptr, chains, start, false, seed_base);
+  // every chain's history is recorded (and stays in HBM), as the reference records one
+  // for every chain (anneal.py:123-213)
+  int rc = run_fused(k, cfg, nullptr, chains, start, true, seed_base);
   if (rc != SIP_OK) return rc;
   sip_ctx* ctx = k->ctx;
   sip_chains& o = *k->ws;
@@ -1411,6 +1646,7 @@ int sip_anneal_epoch(sip_kernel* k, const sip_anneal_cfg* cfg, int64_t seed_base
   if (e == cudaSuccess) e = cudaMemcpyAsync(result, d_res, sizeof *result, cudaMemcpyDeviceToHost, ctx->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
   if (e != cudaSuccess) return fail(ctx, SIP_E_CUDA, std::string("anneal epoch: ") + cudaGetErrorString(e));
+  TRY(ensure_best(ctx, o.s, result->champion_chain, 1));
   SIP_CUDA(ctx, cudaMemcpyAsync(champion, o.s.best + (size_t)result->champion_chain * o.s.ns,
                                 sizeof(uint16_t) * o.s.n, cudaMemcpyDeviceToHost, ctx->stream));
   SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
@@ -1535,9 +1771,24 @@ int sip_results_fetch(sip_results* r, int32_t first, int32_t count, sip_record* 
   Chains& s = r->ws->s;
   if (count == 0) return SIP_OK;
   if (history) TRY(fetch_history(ctx, s, first, count, history));
+  if (best) TRY(ensure_best(ctx, s, first, count));
   if (best) TRY(fetch_sched(ctx, s.best + (size_t)first * s.ns, s.n, s.ns, count, best));
   if (current) TRY(fetch_sched(ctx, s.sched + (size_t)first * s.ns, s.n, s.ns, count, current));
   SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return SIP_OK;
+}
+
+int sip_anneal_state_bytes(sip_kernel* k, int32_t budget, int64_t* per_chain) {
+  if (!k || !per_chain || budget < 0) return SIP_E_ARG;
+  const int64_t n = k->d.n, ns = (n + 7) & ~7, kk = std::max(k->d.k, 1), B = std::max(budget, 1);
+  const int64_t nck = (n + CK - 1) / CK, nck4 = (nck + 3) & ~3, nck8 = (nck + 7) & ~7;
+  const int64_t offp = nck8 + ((((nck + 7) >> 3) + 3) & ~3);
+  *per_chain = 2 * ns * 2                 // sched, best
+               + 4 * (int64_t)MT_N        // MT words
+               + 2 * kk                   // candidate positions
+               + 32 * nck + 4 * offp + 4 * nck4  // checkpoints, offsets, interval masks
+               + 2 * B + (int64_t)sizeof(sip_record) * B  // accepted-swap log, history
+               + 8 * 3 + 4 * 8 + 8 + 2 + 1;     // scalars (t0, energies, counters, seed, ...)
   return SIP_OK;
 }
 
@@ -1547,10 +1798,12 @@ int sip_anneal_wave(sip_kernel* k, int32_t* chains) {
   SIP_CUDA(ctx, cudaSetDevice(ctx->device));
   size_t sm = smem_need(k->d);
   int use_smem = sm <= kSmemCap;
-  if (use_smem) TRY(configure_smem(ctx, (const void*)anneal_fused_kernel, sm));
+  if (use_smem) TRY(configure_smem(ctx, (const void*)anneal_fused_kernel<true>, sm));
   int per_sm = 0;
-  SIP_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, anneal_fused_kernel, 128,
-                                                              use_smem ? sm : 0));
+  if (use_smem)
+    SIP_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, anneal_fused_kernel<true>, 128, sm));
+  else
+    SIP_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, anneal_fused_kernel<false>, 128, 0));
   *chains = per_sm * ctx->sm_count * 128;
   return SIP_OK;
 }

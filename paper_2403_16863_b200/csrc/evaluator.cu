@@ -639,6 +639,22 @@ static int measure_batch_impl(sip_module* m, const uint16_t* perm_ref, const uin
                               const sip_launch* L, int32_t warmup, int32_t reps, int32_t flush_l2,
                               double* ratio_median, double* ref_median_ms, double* cand_median_ms,
                               double* raw_ratio, int32_t* status);
+static int measure_round_impl(sip_module* m, const uint16_t* perm_ref, const uint16_t* perms, int32_t k,
+                              const sip_launch* L, int32_t nL, int32_t warmup, int32_t reps, int32_t flush_l2,
+                              double* ratio_median, double* ref_median_ms, double* cand_median_ms,
+                              double* raw_ratio, int32_t* status);
+
+int sip_measure_round(sip_module* m, const uint16_t* perm_ref, const uint16_t* perms, int32_t k,
+                      const sip_launch* L, int32_t nL, int32_t warmup, int32_t reps, int32_t flush_l2,
+                      double* ratio_median, double* ref_median_ms, double* cand_median_ms,
+                      double* raw_ratio, int32_t* status) {
+  if (!m || !L || nL < 1 || !m->ctx || !perms || k < 1 || !ratio_median || !status || reps < 1 || warmup < 0)
+    return SIP_E_ARG;
+  const int rc = measure_round_impl(m, perm_ref, perms, k, L, nL, warmup, reps, flush_l2, ratio_median,
+                                    ref_median_ms, cand_median_ms, raw_ratio, status);
+  for (auto& c : m->cache) c.pinned = false;
+  return rc;
+}
 
 int sip_measure_paired_batch(sip_module* m, const uint16_t* perm_ref, const uint16_t* perms, int32_t k,
                              const sip_launch* L, int32_t warmup, int32_t reps, int32_t flush_l2,
@@ -654,18 +670,19 @@ int sip_measure_paired_batch(sip_module* m, const uint16_t* perm_ref, const uint
 
 }  // extern "C"
 
-static int measure_batch_impl(sip_module* m, const uint16_t* perm_ref, const uint16_t* perms, int32_t k,
-                              const sip_launch* L, int32_t warmup, int32_t reps, int32_t flush_l2,
-                              double* ratio_median, double* ref_median_ms, double* cand_median_ms,
-                              double* raw_ratio, int32_t* status) {
+// the reference module and every candidate's module of a batch, loaded (cache misses in
+// parallel, SIP_LOAD_THREADS host threads) and pinned in the cache for the batch
+static int load_batch(sip_module* m, const uint16_t* perm_ref, const uint16_t* perms, int32_t k,
+                      CachedMod** ref_out, std::vector<CachedMod*>& mods, int32_t* status) {
   sip_ctx* ctx = m->ctx;
   if (m->cache_cap < (size_t)k + 1) m->cache_cap = (size_t)k + 1;
   CachedMod* ref = nullptr;
   int rc = get_module(m, perm_ref, &ref);
   if (rc != SIP_OK) return rc;
   ref->pinned = true;  // held by every pair of this batch
+  *ref_out = ref;
   // images + parallel cuModuleLoadData for the candidates not loaded yet
-  std::vector<CachedMod*> mods(k, nullptr);
+  mods.assign(k, nullptr);
   std::vector<int> todo;
   for (int i = 0; i < k; ++i) {
     const uint16_t* p = perms + (size_t)i * m->n;
@@ -720,6 +737,18 @@ static int measure_batch_impl(sip_module* m, const uint16_t* perm_ref, const uin
     if (m->cache.size() >= m->cache_cap) evict_one(m);  // the oldest module not in this batch
     mods[i] = insert_module(m, std::move(cm));
   }
+  return SIP_OK;
+}
+
+static int measure_batch_impl(sip_module* m, const uint16_t* perm_ref, const uint16_t* perms, int32_t k,
+                              const sip_launch* L, int32_t warmup, int32_t reps, int32_t flush_l2,
+                              double* ratio_median, double* ref_median_ms, double* cand_median_ms,
+                              double* raw_ratio, int32_t* status) {
+  sip_ctx* ctx = m->ctx;
+  CachedMod* ref = nullptr;
+  std::vector<CachedMod*> mods;
+  int rc = load_batch(m, perm_ref, perms, k, &ref, mods, status);
+  if (rc != SIP_OK) return rc;
   if (flush_l2 && (rc = ensure_flush(ctx)) != SIP_OK) return rc;
   const int nev = 4 * reps * k;
   while ((int)m->events.size() < nev) {
@@ -768,6 +797,91 @@ static int measure_batch_impl(sip_module* m, const uint16_t* perm_ref, const uin
     }
     ratio_median[i] = median_of(ratio);
     if (ref_median_ms) ref_median_ms[i] = median_of(tr);
+    if (cand_median_ms) cand_median_ms[i] = median_of(tc);
+    if (raw_ratio) std::copy(ratio.begin(), ratio.end(), raw_ratio + (size_t)i * reps);
+  }
+  if (exec) cudaGraphExecDestroy(exec);
+  cudaGraphDestroy(graph);
+  if (ce != cudaSuccess)
+    return sip::fail(ctx, SIP_E_MEASURE, std::string("timed launches: ") + cudaGetErrorString(ce));
+  return SIP_OK;
+}
+
+// One nvcc reference per round: the k candidates and the reference
+// are warmed up once each, then every rep launches all k+1 modules once in an order
+// rotated by one slot per rep, each launch bracketed by an event pair.  Launch slot q of
+// the graph uses parameter set L[q % nL]: with nL >= 3 buffer sets larger than L2 in
+// rotation, no launch finds its inputs in L2 and no flush is needed (flush_l2 = 0); with
+// flush_l2 the 256 MB memset precedes every timed launch as before.  A candidate's energy
+// is the median over reps of its time / the reference's time in the same rep.
+static int measure_round_impl(sip_module* m, const uint16_t* perm_ref, const uint16_t* perms, int32_t k,
+                              const sip_launch* L, int32_t nL, int32_t warmup, int32_t reps, int32_t flush_l2,
+                              double* ratio_median, double* ref_median_ms, double* cand_median_ms,
+                              double* raw_ratio, int32_t* status) {
+  sip_ctx* ctx = m->ctx;
+  CachedMod* ref = nullptr;
+  std::vector<CachedMod*> mods;
+  int rc = load_batch(m, perm_ref, perms, k, &ref, mods, status);
+  if (rc != SIP_OK) return rc;
+  if (flush_l2 && (rc = ensure_flush(ctx)) != SIP_OK) return rc;
+  // the round's modules: slot 0 = the reference, then the loadable candidates
+  std::vector<CachedMod*> set{ref};
+  std::vector<int> cand_of;  // set index -> candidate index
+  cand_of.push_back(-1);
+  for (int i = 0; i < k; ++i)
+    if (status[i] == SIP_OK) {
+      set.push_back(mods[i]);
+      cand_of.push_back(i);
+    }
+  const int nm = (int)set.size();
+  const int nev = 2 * reps * nm;
+  while ((int)m->events.size() < nev) {
+    cudaEvent_t e;
+    SIP_CUDA(ctx, cudaEventCreate(&e));
+    m->events.push_back(e);
+  }
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int slot = 0;
+  SIP_CUDA(ctx, cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  for (int w = 0; w < warmup && rc == SIP_OK; ++w)
+    for (int q = 0; q < nm && rc == SIP_OK; ++q) rc = launch(m, set[q], &L[slot++ % nL]);
+  for (int r = 0; r < reps && rc == SIP_OK; ++r)
+    for (int q = 0; q < nm && rc == SIP_OK; ++q) {
+      const int j = (q + r) % nm;  // rotate the order every rep
+      const int e = 2 * (r * nm + j);
+      if (flush_l2) cudaMemsetAsync(ctx->flush_buf, (r * nm + q) & 0xff, ctx->flush_bytes, ctx->stream);
+      cudaEventRecordWithFlags(m->events[e], ctx->stream, cudaEventRecordExternal);
+      rc = launch(m, set[j], &L[slot++ % nL]);
+      cudaEventRecordWithFlags(m->events[e + 1], ctx->stream, cudaEventRecordExternal);
+    }
+  cudaError_t ce = cudaStreamEndCapture(ctx->stream, &graph);
+  if (rc != SIP_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  if (ce != cudaSuccess) return sip::fail(ctx, SIP_E_MEASURE, std::string("capture: ") + cudaGetErrorString(ce));
+  ce = cudaGraphInstantiate(&exec, graph, 0);
+  if (ce == cudaSuccess) ce = cudaGraphLaunch(exec, ctx->stream);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(ctx->stream);
+  std::vector<double> tref(reps);
+  for (int r = 0; r < reps && ce == cudaSuccess; ++r) {
+    float a = 0.f;
+    ce = cudaEventElapsedTime(&a, m->events[2 * r * nm], m->events[2 * r * nm + 1]);
+    tref[r] = a;
+  }
+  for (int q = 1; q < nm && ce == cudaSuccess; ++q) {
+    const int i = cand_of[q];
+    std::vector<double> tc(reps), ratio(reps);
+    for (int r = 0; r < reps && ce == cudaSuccess; ++r) {
+      float b = 0.f;
+      const int e = 2 * (r * nm + q);
+      ce = cudaEventElapsedTime(&b, m->events[e], m->events[e + 1]);
+      tc[r] = b;
+      ratio[r] = b / tref[r];
+    }
+    ratio_median[i] = median_of(ratio);
+    if (ref_median_ms) ref_median_ms[i] = median_of(tref);
     if (cand_median_ms) cand_median_ms[i] = median_of(tc);
     if (raw_ratio) std::copy(ratio.begin(), ratio.end(), raw_ratio + (size_t)i * reps);
   }

@@ -112,6 +112,7 @@ _SIGS = {
                           ctypes.c_int),
     "sip_results_destroy": ([ctypes.c_void_p], ctypes.c_int),
     "sip_anneal_wave": ([ctypes.c_void_p, c_i32p], ctypes.c_int),
+    "sip_anneal_state_bytes": ([ctypes.c_void_p, ctypes.c_int32, c_i64p], ctypes.c_int),
     "sip_host_alloc": ([ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
     "sip_host_free": ([ctypes.c_void_p], ctypes.c_int),
     "sip_chains_create": ([ctypes.c_void_p, ctypes.POINTER(AnnealCfg), c_i64p, c_dblp,
@@ -396,6 +397,12 @@ class DeviceKernel:
         """Chains filling every SM once with the fused kernel (sip_anneal_wave)."""
         v = ctypes.c_int32()
         self.ctx.check(self.ctx.lib.sip_anneal_wave(self.handle, ctypes.byref(v)))
+        return int(v.value)
+
+    def state_bytes(self, budget: int) -> int:
+        """HBM bytes one fused chain keeps (sip_anneal_state_bytes)."""
+        v = ctypes.c_int64()
+        self.ctx.check(self.ctx.lib.sip_anneal_state_bytes(self.handle, int(budget), ctypes.byref(v)))
         return int(v.value)
 
     def anneal_keep(self, seeds, temps: np.ndarray, start=None, unsafe: bool = False,
