@@ -444,24 +444,27 @@ def hardware_phase(kind, listing, local, rank, world, dist, args, rounds, shape=
                                 "the timed region)" if sustained else
                                 "MEASURED_PEAKS.json bf16_tflops (burst)") if pk["src"] == "measured"
                 else "fallback 1590 TFLOP/s"}
-    # the evaluator's device work per candidate: (warmup + reps) launches of each schedule
-    # of the pair, plus the 256 MB L2 flush before every timed launch
-    # the warm-up launches run without a flush before them, i.e. on a warm L2: time them so
-    flush_ms = time_flush(local)
+    # the evaluator roofline of SURVEY s8d config 4: (warmup + reps) launches of the kernel per
+    # candidate, nothing else -- 1 / ((warmup + reps) * T_kernel) candidates/s per GPU
     warm_ms = warm_launch_ms(be, n)
-    npair = 2 if be.paired else 1
-    floor_ms = (npair * be.warmup * warm_ms
-                + npair * hcfg.measure_reps * (avg_ms + flush_ms))
-    hw = {"candidates_per_s": h_eval / (h_ms / 1e3), "rounds": rounds, "chains_per_gpu": args.chains,
+    floor_ms = (be.warmup + hcfg.measure_reps) * avg_ms
+    rate = h_eval / (h_ms / 1e3)
+    hw = {"candidates_per_s": rate, "rounds": rounds, "chains_per_gpu": args.chains,
           "candidate_classes": args.classes, "candidates_in_listing": int(hs.dk.k),
           "proposals": rounds * args.chains * world, "priced": int(h_eval),
           "evaluator_roofline_candidates_per_s": world * 1e3 / floor_ms,
-          "device_busy_frac": (h_eval / (h_ms / 1e3)) / (world * 1e3 / floor_ms),
-          "flush_ms": flush_ms, "warm_launch_ms": warm_ms,
-          "note": "one candidate = re-encode + cuModuleLoadData (8 host threads) + 2 warmup + 5 timed "
-                  "(nvcc, candidate) launch pairs, L2 flushed before each timed launch; a round's "
-                  "candidates share one CUDA graph; energy = median pair ratio; roofline = device "
-                  "time of those 14 launches (the 4 warm-up ones on a warm L2) + 10 flushes"}
+          "device_busy_frac": rate / (world * 1e3 / floor_ms),
+          "t_kernel_ms": avg_ms, "warm_launch_ms": warm_ms,
+          "cold_input_sets": be.nsets,
+          "note": ("one round = the live chains' candidates re-encoded and loaded with cuModuleLoadData "
+                   "(8 host threads), then ONE CUDA graph: every candidate and one nvcc reference warmed "
+                   "up (2 launches each) and launched 5 times in rotated order with an event pair each; "
+                   "energy = median over reps of t_cand / t_ref in the same rep. Launches rotate over "
+                   f"{be.nsets} input sets so no launch finds its inputs in L2 (no flush). Roofline = "
+                   "1 / ((warmup + reps) * T_kernel), T_kernel = average timed launch")}
+    if not be.nsets:
+        hw["note"] += "; this target needs a 256 MB L2 flush before every timed launch instead"
+        hw["flush_ms"] = time_flush(local)
     res = hs.result()
     if dist:
         hs.exchange()
@@ -644,14 +647,16 @@ def main() -> None:
         e1.synchronize()
         e_ms = allreduce(dist, [e0.elapsed_time(e1)], MAX)[0]
         e_priced = allreduce(dist, [ep_priced], SUM)[0]
-        # per step: the seed array and the temperature schedule go down; the listing's tables
-        # are cached on the device per table set (anneal.device_kernel) and are not re-sent
+        # per step: the temperature schedule goes down (consecutive seeds are generated on the
+        # device; the listing's tables are cached per table set, anneal.device_kernel); the
+        # device-reduced champion record, the champion's summary and its best schedule come up
         e2e = {"value": e_priced / (e_ms / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": int(C * 8 + len(temps) * 8),
-               "d2h_bytes_per_step": int(C * 48 + len(temps) * 16 + 2 * n * 2),
+               "h2d_bytes_per_step": int(len(temps) * 8),
+               "d2h_bytes_per_step": int(48 + 48 + 2 * n),
                "api": "run_search(kernel, SimulatorBackend(), AnnealConfig(seed), chains=C) per step; "
-                      "per-chain histories/schedules stay in HBM until accessed (the champion's are "
-                      "fetched every step)"}
+                      "the champion (driver.py:81-85 ranking) is reduced on the device; per-chain "
+                      "summaries, histories and schedules stay in HBM until accessed (the champion's "
+                      "summary and best schedule are fetched every step)"}
 
     # ================= phase B: hardware evaluator on the tuning targets =================
     gemm = hardware_phase("gemm", listing, local, rank, world, dist, args, rounds=args.hw_steps)

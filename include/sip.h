@@ -159,6 +159,14 @@ int sip_anneal_epoch(sip_kernel* k, const sip_anneal_cfg* cfg, int64_t seed_base
                      const uint16_t* start, sip_epoch_result* result, uint16_t* champion);
 int sip_anneal_keep(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds, int32_t chains,
                     const uint16_t* start, sip_chain_summary* summary, sip_results** out);
+/* sip_anneal_keep without the summaries: seeds given, or seed_base + c generated on the
+ * device when `seeds` is NULL (run_search's consecutive seeds, driver.py:73-79); the
+ * champion under driver.py:81-85's ranking and the sums come back reduced on the device,
+ * per-chain summaries stay in HBM until sip_results_summary reads a range of them. */
+int sip_anneal_keep_reduced(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds, int64_t seed_base,
+                            int32_t chains, const uint16_t* start, sip_epoch_result* result,
+                            sip_results** out);
+int sip_results_summary(sip_results* r, int32_t first, int32_t count, sip_chain_summary* summary);
 int sip_results_fetch(sip_results* r, int32_t first, int32_t count, sip_record* history,
                       uint16_t* best, uint16_t* current);
 int sip_results_destroy(sip_results* r);

@@ -249,19 +249,36 @@ def device_kernel(kernel: Kernel, machine: MachineConfig | None = None, tables: 
 class BatchStates:
     """The AnnealStates of one fused launch, built on access (a read-only list).
 
-    Summaries (energies, baseline, priced counts) are on the host; records and
-    schedules stay in HBM until a state's history / best / current is read.
+    Records, schedules and per-chain summaries stay in HBM until read: a state's
+    energies come with its first access (one 48-byte summary), its history / best /
+    current with theirs.  The champion and the priced total were reduced on the device.
     """
 
-    def __init__(self, kernel: Kernel, summ, res, temps):
+    def __init__(self, kernel: Kernel, reduced: dict, res, temps):
         self.kernel = kernel
-        self.summ = summ
+        self.reduced = reduced
         self.res = res
         self.temps = temps
+        self._summ = None
         self._states: dict = {}
 
+    @property
+    def summ(self) -> np.ndarray:
+        """Every chain's summary (one device->host copy on first use)."""
+        if self._summ is None:
+            self._summ = self.res.summary()
+        return self._summ
+
+    def summary_of(self, c: int):
+        return self._summ[c] if self._summ is not None else self.res.summary(c, 1)[0]
+
+    @property
+    def champion(self) -> int:
+        """Chain index of the best (best energy, seed) -- driver.py:81-85's ranking."""
+        return int(self.reduced["champion_chain"])
+
     def __len__(self) -> int:
-        return len(self.summ)
+        return self.res.C
 
     def __getitem__(self, c):
         if isinstance(c, slice):
@@ -272,7 +289,7 @@ class BatchStates:
             raise IndexError(c)
         st = self._states.get(c)
         if st is None:
-            sm = self.summ[c]
+            sm = self.summary_of(c)
             st = AnnealState(None, float(sm["best_energy"]), None, float(sm["current_energy"]),
                              float(sm["t0"]), "cycles", len(self.temps), temps=self.temps,
                              base=self.kernel, device=(self.res, c), priced=int(sm["priced"]),
@@ -285,7 +302,7 @@ class BatchStates:
 
     @property
     def priced_total(self) -> int:
-        return int(self.summ["priced"].sum())
+        return int(self.reduced["priced"])
 
 
 def anneal_batch_sim(kernel: Kernel, machine: MachineConfig, cfg: AnnealConfig, seeds,
@@ -295,11 +312,14 @@ def anneal_batch_sim(kernel: Kernel, machine: MachineConfig, cfg: AnnealConfig, 
         raise NoCandidatesError("no global-memory instructions to move")
     dk = device_kernel(kernel, machine, tables, cfg.candidate_classes)
     temps = cfg.temperatures()
-    summ, res = dk.anneal_keep(seeds, temps, unsafe=cfg.unsafe_moves, hw_safe=cfg.hw_safe,
-                               min_fixed=cfg.min_fixed_distance)
-    if len(summ) and float(summ["t0"].min()) <= 0:
-        raise InvalidBaseline(f"baseline measurement {float(summ['t0'].min())} is not positive")
-    return BatchStates(kernel, summ, res, temps)
+    reduced, res = dk.anneal_keep_reduced(seeds, temps, unsafe=cfg.unsafe_moves, hw_safe=cfg.hw_safe,
+                                          min_fixed=cfg.min_fixed_distance)
+    states = BatchStates(kernel, reduced, res, temps)
+    if len(states):  # every chain's t0 is the listing's baseline (anneal.py:141-143)
+        t0 = float(states[states.champion].baseline)
+        if t0 <= 0:
+            raise InvalidBaseline(f"baseline measurement {t0} is not positive")
+    return states
 
 
 def anneal_steps(kernel: Kernel, backend, cfg: AnnealConfig, seeds, *,

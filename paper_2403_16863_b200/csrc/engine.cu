@@ -1623,13 +1623,8 @@ __global__ void __launch_bounds__(256) epoch_final_kernel(const sip_epoch_result
 
 extern "C" {
 
-int sip_anneal_epoch(sip_kernel* k, const sip_anneal_cfg* cfg, int64_t seed_base, int32_t chains,
-                     const uint16_t* start, sip_epoch_result* result, uint16_t* champion) {
-  if (!k || !cfg || !result || !champion) return SIP_E_ARG;
-  // every chain's history is recorded (and stays in HBM), as the reference records one
-  // for every chain (anneal.py:123-213)
-  int rc = run_fused(k, cfg, nullptr, chains, start, true, seed_base);
-  if (rc != SIP_OK) return rc;
+// champion + sums of the fused chains in k->ws, reduced on the device; one 48-byte copy
+static int epoch_reduce(sip_kernel* k, sip_epoch_result* result) {
   sip_ctx* ctx = k->ctx;
   sip_chains& o = *k->ws;
   constexpr int kParts = 256;
@@ -1646,6 +1641,47 @@ int sip_anneal_epoch(sip_kernel* k, const sip_anneal_cfg* cfg, int64_t seed_base
   if (e == cudaSuccess) e = cudaMemcpyAsync(result, d_res, sizeof *result, cudaMemcpyDeviceToHost, ctx->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
   if (e != cudaSuccess) return fail(ctx, SIP_E_CUDA, std::string("anneal epoch: ") + cudaGetErrorString(e));
+  return SIP_OK;
+}
+
+int sip_anneal_keep_reduced(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* seeds, int64_t seed_base,
+                            int32_t chains, const uint16_t* start, sip_epoch_result* result,
+                            sip_results** out) {
+  if (!result || !out) return SIP_E_ARG;
+  int rc = run_fused(k, cfg, seeds, chains, start, true, seed_base);
+  if (rc != SIP_OK) return rc;
+  TRY(epoch_reduce(k, result));
+  auto* r = new sip_results();
+  r->k = k;
+  r->ws = k->ws;  // the workspace now belongs to the result set
+  k->ws = nullptr;
+  *out = r;
+  return SIP_OK;
+}
+
+int sip_results_summary(sip_results* r, int32_t first, int32_t count, sip_chain_summary* summary) {
+  if (!r || !r->ws || !summary || first < 0 || count < 0 || first + count > r->ws->s.C) return SIP_E_ARG;
+  if (count == 0) return SIP_OK;
+  sip_ctx* ctx = r->k->ctx;
+  sip_chains* o = r->ws;
+  if (!o->d_summary) TRY(dalloc(ctx, &o->d_summary, (size_t)o->s.C));
+  pack_summary_kernel<<<(o->s.C + 255) / 256, 256, 0, ctx->stream>>>(o->s, o->d_summary);
+  SIP_CHECK_LAUNCH(ctx);
+  TRY(d2h(ctx, summary, o->d_summary + first, (size_t)count));
+  SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return SIP_OK;
+}
+
+int sip_anneal_epoch(sip_kernel* k, const sip_anneal_cfg* cfg, int64_t seed_base, int32_t chains,
+                     const uint16_t* start, sip_epoch_result* result, uint16_t* champion) {
+  if (!k || !cfg || !result || !champion) return SIP_E_ARG;
+  // every chain's history is recorded (and stays in HBM), as the reference records one
+  // for every chain (anneal.py:123-213)
+  int rc = run_fused(k, cfg, nullptr, chains, start, true, seed_base);
+  if (rc != SIP_OK) return rc;
+  sip_ctx* ctx = k->ctx;
+  sip_chains& o = *k->ws;
+  TRY(epoch_reduce(k, result));
   TRY(ensure_best(ctx, o.s, result->champion_chain, 1));
   SIP_CUDA(ctx, cudaMemcpyAsync(champion, o.s.best + (size_t)result->champion_chain * o.s.ns,
                                 sizeof(uint16_t) * o.s.n, cudaMemcpyDeviceToHost, ctx->stream));

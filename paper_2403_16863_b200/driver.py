@@ -145,16 +145,14 @@ def run_search(kernel: Kernel, backend, anneal_cfg: AnnealConfig, *, chains: int
         digest = kernel.__dict__["_input_hash"] = input_hash(serialize_kernel(kernel))
     states = run_states(kernel, backend, anneal_cfg, chains, _tester(kernel, plan, anneal_cfg),
                         on_epoch=on_epoch)
-    if plan is None and store is None and hasattr(states, "summ"):
-        # batched simulator search: rank on the device summaries, build outcomes on access
-        summ = states.summ
-        times = summ["best_energy"] * summ["t0"]
+    if plan is None and store is None and hasattr(states, "champion"):
+        # batched simulator search: the champion under (best_time, seed) (driver.py:81-85)
+        # was reduced on the device -- every chain shares t0, so best_time orders like the
+        # best energy; per-chain outcomes are built on access
         lazy = LazyOutcomes(states, anneal_cfg.seed)
-        # (best_time, seed) ranking (driver.py:81-85): seeds increase with the chain
-        # index, so the first minimum is the champion -- O(C) instead of a sort
-        best = lazy[int(np.argmin(times))] if len(summ) else None
-        baseline = float(summ["t0"][-1]) if len(summ) else 0.0
-        return SearchReport(kernel, digest, baseline, "cycles", lazy, best, len(candidates(kernel)))
+        best = lazy[states.champion] if len(states) else None
+        baseline = float(best.state.baseline) if best is not None else 0.0
+        return SearchReport(kernel, digest, baseline, "cycles", lazy, best, len(candidates(kernel, anneal_cfg.candidate_classes)))
     outcomes = []
     for c, st in enumerate(states):
         verdict = None
@@ -177,4 +175,4 @@ def run_search(kernel: Kernel, backend, anneal_cfg: AnnealConfig, *, chains: int
                             "iterations": o.state.iterations})
         store.update_manifest(digest, baseline=baseline, unit=unit, entries=entries)
 
-    return SearchReport(kernel, digest, baseline, unit, outcomes, best, len(candidates(kernel)))
+    return SearchReport(kernel, digest, baseline, unit, outcomes, best, len(candidates(kernel, anneal_cfg.candidate_classes)))

@@ -111,6 +111,10 @@ _SIGS = {
     "sip_results_fetch": ([ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, c_u16p, c_u16p],
                           ctypes.c_int),
     "sip_results_destroy": ([ctypes.c_void_p], ctypes.c_int),
+    "sip_anneal_keep_reduced": ([ctypes.c_void_p, ctypes.POINTER(AnnealCfg), c_i64p, ctypes.c_int64,
+                                 ctypes.c_int32, c_u16p, ctypes.POINTER(EpochResult),
+                                 ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "sip_results_summary": ([ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p], ctypes.c_int),
     "sip_anneal_wave": ([ctypes.c_void_p, c_i32p], ctypes.c_int),
     "sip_anneal_state_bytes": ([ctypes.c_void_p, ctypes.c_int32, c_i64p], ctypes.c_int),
     "sip_host_alloc": ([ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
@@ -136,6 +140,9 @@ _SIGS = {
     "sip_measure_paired_batch": ([ctypes.c_void_p, c_u16p, c_u16p, ctypes.c_int32, ctypes.POINTER(Launch),
                                   ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, c_dblp, c_dblp, c_dblp,
                                   c_dblp, c_i32p], ctypes.c_int),
+    "sip_measure_round": ([ctypes.c_void_p, c_u16p, c_u16p, ctypes.c_int32, ctypes.POINTER(Launch),
+                           ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, c_dblp, c_dblp,
+                           c_dblp, c_dblp, c_i32p], ctypes.c_int),
     "sip_run": ([ctypes.c_void_p, c_u16p, ctypes.POINTER(Launch)], ctypes.c_int),
     "sip_run_async": ([ctypes.c_void_p, c_u16p, ctypes.POINTER(Launch)], ctypes.c_int),
     "sip_verify_open": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p)],
@@ -420,6 +427,26 @@ class DeviceKernel:
             None if st is None else _ptr(st, c_u16p), summ.ctypes.data_as(ctypes.c_void_p), ctypes.byref(h)))
         return summ, DeviceResults(self, h, C, len(temps))
 
+    def anneal_keep_reduced(self, seeds, temps: np.ndarray, start=None, unsafe: bool = False,
+                            hw_safe: bool = False, min_fixed: int = 0):
+        """Fused chains left entirely in HBM (sip_anneal_keep_reduced): only the device-reduced
+        champion and sums come back; consecutive seeds are generated on the device.
+        Returns (EpochResult dict, DeviceResults)."""
+        seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.int64))
+        temps = np.ascontiguousarray(temps, dtype=np.float64)
+        C = len(seeds)
+        consecutive = C > 0 and (C == 1 or bool(np.all(np.diff(seeds) == 1)))
+        st = None if start is None else np.ascontiguousarray(start, dtype=np.uint16)
+        cfg = self._cfg(temps, unsafe, hw_safe, min_fixed)
+        res = EpochResult()
+        h = ctypes.c_void_p()
+        self.ctx.check(self.ctx.lib.sip_anneal_keep_reduced(
+            self.handle, ctypes.byref(cfg), None if consecutive else _ptr(seeds, c_i64p),
+            int(seeds[0]) if consecutive else 0, C, None if st is None else _ptr(st, c_u16p),
+            ctypes.byref(res), ctypes.byref(h)))
+        out = {f: getattr(res, f) for f, _ in EpochResult._fields_ if f != "pad"}
+        return out, DeviceResults(self, h, C, len(temps))
+
     def chains(self, seeds, t0, temps: np.ndarray, unsafe: bool = False, hw_safe: bool = False,
                min_fixed: int = 0) -> "StepChains":
         return StepChains(self, seeds, t0, temps, unsafe, hw_safe, min_fixed)
@@ -485,6 +512,14 @@ class DeviceResults:
         self.C = chains
         self.budget = budget
         self._cache: dict = {}
+
+    def summary(self, first: int = 0, count: int | None = None) -> np.ndarray:
+        """Per-chain summaries [first, first + count) (sip_results_summary)."""
+        count = self.C - first if count is None else count
+        out = pinned_pool(self.dk.ctx.lib).records(count, SUMMARY_DTYPE)
+        ctx = self.dk.ctx
+        ctx.check(ctx.lib.sip_results_summary(self.handle, first, count, out.ctypes.data_as(ctypes.c_void_p)))
+        return out
 
     def fetch(self, c: int):
         """(records[budget], best[n], current[n]) of chain c."""

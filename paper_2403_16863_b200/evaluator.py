@@ -17,9 +17,9 @@ import numpy as np
 
 from .backends import BackendDescriptor, CostSample, MeasurementFailed
 from .cubin import Listing, Module, render_listing, schedule_perm
-from .engine import SIP_E_MEASURE, EngineError, c_dblp, c_i32p, c_u16p, get_context
+from .engine import SIP_E_MEASURE, EngineError, Launch, c_dblp, c_i32p, c_u16p, get_context
 from .ir import Kernel
-from .targets import make_target
+from .targets import cold_sets, launch_sets, make_target
 
 FIXED_LAT_HEAVY = ("HMMA", "IMMA", "DMMA", "BMMA", "HGMMA", "DFMA", "DADD", "DMUL")
 
@@ -38,7 +38,7 @@ class B200Backend:
     hardware = True        # candidates execute on the GPU: hw_safe legality is enforced
 
     def __init__(self, target, listing: Listing | None = None, *, device: int = 0, warmup: int = 2,
-                 flush_l2: bool = True, paired: bool = True):
+                 flush_l2: bool = True, paired: bool = True, rounds: bool = True):
         self.target = target
         self.device = device
         self.ctx = get_context(device)
@@ -54,6 +54,12 @@ class B200Backend:
         # paired mode: every candidate is timed against the nvcc schedule inside the same
         # graph; its value is (median cand/ref ratio) x the reference time measured here
         self.paired = paired
+        # round mode (measure_batch): one nvcc reference per round of candidates, launches
+        # rotated over input sets larger than L2 (targets.cold_sets) instead of a flush
+        self.rounds = rounds and paired
+        self.nsets = cold_sets(target) if self.rounds else 0
+        self._sets = launch_sets(target, self.nsets) if self.nsets else []
+        self._set_array = (Launch * max(1, len(self._sets)))(*[lp for lp, _ in self._sets]) if self._sets else None
         self.identity = np.arange(self.listing.n, dtype=np.uint16)
         self.ref_ms = self._measure_single(self.identity, 9).value if paired else None
 
@@ -122,21 +128,33 @@ class B200Backend:
         raw = np.zeros((k, reps), dtype=np.float64)
         status = np.zeros(k, dtype=np.int32)
         lib = self.ctx.lib
-        rc = lib.sip_measure_paired_batch(
-            self.module.handle, self.identity.ctypes.data_as(c_u16p), perms.ctypes.data_as(c_u16p), k,
-            ctypes.byref(self.launch), self.warmup, reps, int(self.flush_l2), ratio.ctypes.data_as(c_dblp),
-            refm.ctypes.data_as(c_dblp), candm.ctypes.data_as(c_dblp), raw.ctypes.data_as(c_dblp),
-            status.ctypes.data_as(c_i32p))
+        if self.rounds:
+            # one reference per round; cold inputs by rotation (nsets > 0) or a flush
+            sets, nL = ((self._set_array, len(self._sets)) if self.nsets
+                        else (ctypes.pointer(self.launch), 1))
+            rc = lib.sip_measure_round(
+                self.module.handle, self.identity.ctypes.data_as(c_u16p), perms.ctypes.data_as(c_u16p), k,
+                sets, nL, self.warmup, reps, int(self.flush_l2 and not self.nsets),
+                ratio.ctypes.data_as(c_dblp), refm.ctypes.data_as(c_dblp), candm.ctypes.data_as(c_dblp),
+                raw.ctypes.data_as(c_dblp), status.ctypes.data_as(c_i32p))
+        else:
+            rc = lib.sip_measure_paired_batch(
+                self.module.handle, self.identity.ctypes.data_as(c_u16p), perms.ctypes.data_as(c_u16p), k,
+                ctypes.byref(self.launch), self.warmup, reps, int(self.flush_l2), ratio.ctypes.data_as(c_dblp),
+                refm.ctypes.data_as(c_dblp), candm.ctypes.data_as(c_dblp), raw.ctypes.data_as(c_dblp),
+                status.ctypes.data_as(c_i32p))
         self.calls += k
         if rc == SIP_E_MEASURE:
             raise MeasurementFailed(lib.sip_last_error(self.ctx.handle).decode(errors="replace"))
         self.ctx.check(rc)
         out = []
+        if self.rounds and (status == 0).any():
+            self.kernel_ms.extend([float(refm[status == 0][0])] * reps)  # the round's one reference
         for i in range(k):
             if status[i] != 0:
                 out.append(MeasurementFailed(f"candidate {i}: cubin could not be loaded"))
                 continue
-            self.kernel_ms.extend([float(refm[i])] * reps + [float(candm[i])] * reps)
+            self.kernel_ms.extend(([] if self.rounds else [float(refm[i])] * reps) + [float(candm[i])] * reps)
             out.append(CostSample(float(ratio[i]) * self.ref_ms, self.unit, reps,
                                   tuple(float(r) * self.ref_ms for r in raw[i])))
         return out

@@ -71,7 +71,9 @@ class HardwareSearch:
             self.times[c] = smp.value
             self.status[c] = ST_PRICED
             n += 1
-            self.launches += 2 * (self.be.warmup + self.cfg.measure_reps)
+            self.launches += (1 if getattr(self.be, "rounds", False) else 2) * (self.be.warmup + self.cfg.measure_reps)
+        if n and getattr(self.be, "rounds", False):
+            self.launches += self.be.warmup + self.cfg.measure_reps  # the round's one nvcc reference
         if len(live):
             self.chains.resolve(self.times, self.status)
             self.launches += 1

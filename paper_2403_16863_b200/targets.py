@@ -112,6 +112,34 @@ class GemmTarget:
         return torch.where(y > 0, y, y * self.slope)
 
 
+L2_BYTES = 126 << 20  # B200 L2
+
+
+def cold_sets(target) -> int:
+    """Independent input sets the evaluator rotates through so that no timed launch finds
+    its inputs in L2: between two uses of a set the other sets' launches stream at least
+    twice the L2 size.  0 means "too many: flush L2 before every timed launch instead"."""
+    per = max(1, int(target.min_bytes))
+    if per >= 2 * L2_BYTES:
+        return 1
+    n = -(-2 * L2_BYTES // per) + 1
+    return n if n <= 64 else 0
+
+
+def launch_sets(target, n: int) -> list:
+    """[(Launch, params)] of `n` input sets: the target's own buffers, then n - 1 sibling
+    targets with their own buffers and Philox streams (kept alive on the target)."""
+    from dataclasses import replace
+
+    sets = [target.launch()]
+    sibs = getattr(target, "_siblings", [])
+    while len(sibs) < n - 1:
+        sibs.append(replace(target, seed=target.seed + 7919 * (len(sibs) + 1), _bufs={}).allocate())
+    target._siblings = sibs
+    sets.extend(t.launch() for t in sibs[: n - 1])
+    return sets
+
+
 TARGET_KINDS = {"gemm": GemmTarget}
 
 

@@ -245,6 +245,27 @@ def test_measure_batch_paired():
         assert 0.8 * be.ref_ms < smp.value < 1.25 * be.ref_ms
 
 
+@pytest.mark.parametrize("shape,rounds", [((2048, 2048, 2048), True), ((512, 512, 1024), False)])
+def test_measure_round_and_legacy_batch(shape, rounds):
+    """sip_measure_round (one nvcc reference per round; 2048^3 rotates over input sets
+    larger than L2 instead of flushing) and the per-candidate paired batch: identical
+    schedules time as ratio ~1 against the reference, the round prices all of them."""
+    from paper_2403_16863_b200.targets import cold_sets
+
+    M, N, K = shape
+    tgt = GemmTarget(M=M, N=N, K=K).allocate()
+    be = B200Backend(tgt, rounds=rounds)
+    if rounds:
+        assert be.nsets == cold_sets(tgt) and be.nsets >= 3
+        assert (be.nsets - 1) * tgt.min_bytes >= 2 * (126 << 20)
+    ident = schedule_perm(be.kernel)
+    out = be.measure_batch(np.stack([ident] * 6), reps=5)
+    assert len(out) == 6
+    for smp in out:
+        assert not isinstance(smp, Exception)
+        assert len(smp.raw) == 5 and 0.9 * be.ref_ms < smp.value < 1.1 * be.ref_ms
+
+
 def test_measure_batch_module_cache_churn():
     """Batches larger than the module cache, repeated, with the baseline schedule itself
     among the candidates: no module a batch still launches may be evicted (a dangling

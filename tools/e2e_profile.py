@@ -5,7 +5,7 @@ from bench import decoded_listing
 from paper_2403_16863_b200 import AnnealConfig, SimulatorBackend, run_search
 from paper_2403_16863_b200.machine import MachineConfig
 L = decoded_listing()
-C = 262144
+C = int(sys.argv[1]) if len(sys.argv) > 1 else 227328
 for k in range(2):
     run_search(L.kernel, SimulatorBackend(MachineConfig()), AnnealConfig(seed=k * C), chains=C).best.state.best_perm
 pr = cProfile.Profile(); pr.enable()
