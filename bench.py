@@ -69,6 +69,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-attn", action="store_true")
     ap.add_argument("--attn-steps", type=int, default=8, help="attention hardware search rounds")
+    ap.add_argument("--no-unmodified", action="store_true",
+                    help="reference arm: skip the unmodified-package lines (baseline/_ref)")
     return ap.parse_args()
 
 
@@ -191,6 +193,39 @@ def engine_roofline(cand_per_s: float, chains: int, state_bytes: int, sm_mhz) ->
             "source": f"profiles/engine_ncu_summary.json ({d.get('source')}); rate and clock from this run"}
 
 
+def engine_at_realistic_k(ctx, gemm_listing, temps, dist, world, steps: int = 3) -> dict:
+    """The same engine and metric with the sm_100 extension classes, where the
+    listings have hundreds of candidates instead of the reference classes' five: the GEMM
+    listing and the attention listing, two full waves of chains each, histories recorded."""
+    import torch
+
+    from paper_2403_16863_b200.cubin import render_listing
+    from paper_2403_16863_b200.machine import MachineConfig
+    from paper_2403_16863_b200.parallel import RED_MAX, RED_SUM
+    from paper_2403_16863_b200.tables import KernelTables
+    from paper_2403_16863_b200.targets import TARGET_DIR
+
+    out = {}
+    attn = render_listing((TARGET_DIR / "attn_fwd.cubin").read_bytes(), "attn_fwd_f16")
+    for name, lst in (("gemm_lrelu_f16", gemm_listing), ("attn_fwd_f16", attn)):
+        dk = ctx.kernel(KernelTables.build(lst.kernel, MachineConfig(), classes="extended"))
+        C = 2 * dk.wave_chains()
+        for w in range(2):
+            dk.anneal_epoch_reduced(10_000_000 + w * C, C, temps)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        priced = 0
+        for k in range(steps):
+            res, _ = dk.anneal_epoch_reduced(20_000_000 + k * C, C, temps)
+            priced += int(res["priced"])
+        torch.cuda.synchronize()
+        sec = allreduce(dist, [time.perf_counter() - t0], RED_MAX)[0]
+        priced = allreduce(dist, [priced], RED_SUM)[0]
+        out[name] = {"candidates_per_s": priced / sec, "n": lst.n, "k": int(dk.k), "chains_per_gpu": C,
+                     "classes": "extended", "priced_per_chain": priced / (world * C * steps)}
+    return out
+
+
 def ncu_traffic(kind: str) -> float | None:
     """dram bytes per launch of a target from its committed ncu --set full summary."""
     p = ROOT / "profiles" / f"{kind}_ncu_summary.json"
@@ -303,7 +338,100 @@ def run_reference(args, rank: int) -> None:
                          "sample": vals[0]["sample"]},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    ref = ROOT / "baseline" / "_ref"
+    if (ref / "sasstune").exists() and not args.no_unmodified:
+        # the unmodified reference package itself (pip-installed into baseline/_ref), beside
+        # the port: its simulator search on all cores, and its hardware loop through its
+        # own ExternalCommandBackend driving the B200 adapter
+        line["unmodified_reference"] = {"simulator": unmodified_sim_rate(20.0, cores)}
+        line["unmodified_reference"]["hw"] = unmodified_hw_rate(90.0)
     print(json.dumps(line), flush=True)
+
+
+REF_LISTING = ROOT / "tests" / "golden" / "listings" / "gemm_lrelu_f16.sass"
+
+
+def _unmodified_worker(wid: int, seconds: float):
+    sys.path.insert(0, str(ROOT / "baseline" / "_ref"))
+    from sasstune import AnnealConfig as RC, MachineConfig as RM, SimulatorBackend as RS
+    from sasstune.driver import run_search as rrun
+    from sasstune.sasstext import parse_kernel as rparse
+
+    kernel = rparse(REF_LISTING.read_text())
+    t0 = time.perf_counter()
+    priced = chains = 0
+    while time.perf_counter() - t0 < seconds:
+        rep = rrun(kernel, RS(RM()), RC(seed=100_000 * wid + chains), chains=1)
+        priced += sum(1 for h in rep.chains[0].state.history if h.energy is not None)
+        chains += 1
+    return priced, chains, time.perf_counter() - t0
+
+
+def unmodified_sim_rate(seconds: float, workers: int) -> dict:
+    """sasstune.run_search (SimulatorBackend, AnnealConfig defaults) on the committed decoded
+    listing, one chain per call, `workers` processes with disjoint seeds (the reference runs
+    its chains sequentially, driver.py:73-79)."""
+    from concurrent.futures import ProcessPoolExecutor
+
+    t0 = time.perf_counter()
+    with ProcessPoolExecutor(workers) as ex:
+        res = list(ex.map(_unmodified_worker, range(workers), [seconds] * workers))
+    wall = time.perf_counter() - t0
+    priced, chains = sum(r[0] for r in res), sum(r[1] for r in res)
+    return {"value": priced / wall, "unit": UNIT, "cores": workers, "chains": chains,
+            "sample": f"{chains} chains of sasstune.run_search on the decoded gemm_lrelu_f16 listing "
+                      f"(n=1184), {workers} processes, {wall:.1f} s wall (includes imports)"}
+
+
+def unmodified_hw_rate(seconds: float) -> dict | None:
+    """sasstune.anneal through its ExternalCommandBackend with the B200 adapter
+    (`python -m paper_2403_16863_b200 measure --target gemm {schedule_file}`, a subprocess per
+    rep as backends.py:66-116 does): the reference's hardware loop on this box.  Bounded by
+    time: once `seconds` have passed every further measurement fails fast (the reference then
+    discards the candidate, anneal.py:186-189) and the rate counts the priced ones."""
+    try:
+        import torch
+
+        if not torch.cuda.is_available():
+            return None
+    except ImportError:
+        return None
+    sys.path.insert(0, str(ROOT / "baseline" / "_ref"))
+    from sasstune import AnnealConfig as RC, ExternalCommandBackend, MeasurementFailed as RMF
+    from sasstune.anneal import anneal as ranneal
+    from sasstune.sasstext import parse_kernel as rparse
+
+    inner = ExternalCommandBackend(f"{sys.executable} -m paper_2403_16863_b200 measure --target gemm "
+                                   "{schedule_file}", timeout_s=300.0, workdir=str(ROOT))
+
+    class Bounded:
+        unit = inner.unit
+
+        def __init__(self):
+            self.t0 = time.perf_counter()
+            self.priced = 0
+            self.busy = 0.0
+
+        def measure(self, kernel, reps=1):
+            if time.perf_counter() - self.t0 > seconds:
+                raise RMF("bench time budget spent")
+            t = time.perf_counter()
+            out = inner.measure(kernel, reps)
+            self.busy += time.perf_counter() - t
+            self.priced += 1
+            return out
+
+    be = Bounded()
+    try:
+        ranneal(rparse(REF_LISTING.read_text()), be, RC(seed=0, t_max=0.02, t_min=0.0005, cooling=1.02,
+                                                         measure_reps=5))
+    except RMF as exc:  # the baseline measurement itself failed
+        return {"error": str(exc)}
+    cands = max(0, be.priced - 1)  # the first measure is the baseline t0
+    return {"candidates_per_s": cands / be.busy if be.busy and cands else 0.0, "priced": cands,
+            "seconds_measuring": be.busy,
+            "what": "unmodified sasstune.anneal + ExternalCommandBackend (5 subprocess reps per "
+                    "candidate) + the B200 adapter; one chain, reference classes"}
 
 
 # ---------------------------------------------------------------------------
@@ -616,6 +744,7 @@ def main() -> None:
               "listing_instructions": n, "candidates_in_listing": int(dk.k),
               "global_best_energy": best["e"], "ambiguous_metropolis": amb}
 
+    engine["realistic_k"] = engine_at_realistic_k(ctx, listing, temps, dist, world)
     engine["roofline"] = engine_roofline(priced_all / world / (ms_all / 1e3), C, dk.state_bytes(len(temps)),
                                          clk.summary().get("sm_mhz"))
 

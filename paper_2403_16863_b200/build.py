@@ -26,7 +26,13 @@ LIB_SOURCES = ["context.cu", "engine.cu", "evaluator.cu", "verify.cu", "interp.c
 CUBINS = {"gemm_lrelu": "gemm_lrelu.cu", "attn_fwd": "attn_fwd.cu", "canary": "canary.cu"}
 # build-time variants for descriptor probes, e.g. {"attn_fwd_vswap": ("attn_fwd.cu", ["-DSIP_VDESC_SWAP"])}
 # (the swapped MN-major LBO/SBO encoding was measured wrong on a B200: max err 0.077 vs 4e-5)
-CUBIN_VARIANTS: dict = {}
+CUBIN_VARIANTS: dict = {
+    # ablations for the per-configuration speed-up bounds (tools/upper_bound.py): the region
+    # holding the movable instructions made free -- no reordering of it can do better
+    "gemm_lrelu_nomath": ("gemm_lrelu.cu", ["-DSIP_DIAG_NOMATH"]),
+    "gemm_lrelu_noepi": ("gemm_lrelu.cu", ["-DSIP_DIAG_NOEPI"]),
+    "attn_fwd_nomath": ("attn_fwd.cu", ["-DSIP_DIAG_NOMATH"]),
+}
 
 
 def _run(cmd, cwd=None) -> None:

@@ -183,21 +183,32 @@ gemm_lrelu_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       tc_fence_after();
       __half* crow = C + ((size_t)l * M + m0 + row_in_tile) * (size_t)N + n0;
       const uint32_t t_base = tmem + ((uint32_t)(quarter * 32) << 16) + buf * ACC_COLS;
+#ifndef SIP_DIAG_NOEPI  // diagnostic build (tools/upper_bound.py): no epilogue at all
 #pragma unroll 1
       for (int c = 0; c < chunks; ++c) {
         uint32_t v[32];
         tmem_ld32(t_base + c * 32, v);
         tmem_ld_wait();
         uint32_t h[16];
+#ifdef SIP_DIAG_NOMATH  // diagnostic build: the epilogue's ALU work (LeakyReLU, packing) removed
+#pragma unroll
+        for (int j = 0; j < 16; ++j) h[j] = v[2 * j];
+#else
 #pragma unroll
         for (int j = 0; j < 16; ++j)
           h[j] = pack_half2(leaky(__uint_as_float(v[2 * j]), slope), leaky(__uint_as_float(v[2 * j + 1]), slope));
+#endif
         __half* dst = crow + c * 32;
         stg128(dst, h[0], h[1], h[2], h[3]);
         stg128(dst + 8, h[4], h[5], h[6], h[7]);
         stg128(dst + 16, h[8], h[9], h[10], h[11]);
         stg128(dst + 24, h[12], h[13], h[14], h[15]);
       }
+#else
+      (void)crow;
+      (void)t_base;
+      (void)chunks;
+#endif
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {

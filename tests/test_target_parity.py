@@ -183,3 +183,31 @@ def test_product_tables_match_reference_facts(name):
     for i in range(t.n):
         for which in ("reads", "writes"):
             assert names(t, i, which, t.names) == names(g, i, which, gorder), (i, which)
+
+
+# the sm_100 extension classes: no reference counterpart, so the device is
+# pinned to the oracle on the extended tables (movable compute, exact packed-pair footprints,
+# every non-movable instruction a fence) -- the engine at realistic candidate counts
+EXT_MANY = {"gemm_lrelu_f16": 1024, "attn_fwd_f16": 256}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", sorted(EXT_MANY))
+def test_device_chains_vs_oracle_extended_classes(name):
+    from paper_2403_16863_b200.engine import get_context
+
+    rec, k, _ = setup(name)
+    t = KernelTables.build(k, MachineConfig(), classes="extended")
+    assert len(t.global_ids) > 300  # hundreds of candidates, not the reference's five
+    dk = get_context().kernel(t)
+    temps = AnnealConfig().temperatures()
+    seeds = np.arange(70_000, 70_000 + EXT_MANY[name], dtype=np.int64)
+    hist, best, cur, summ = dk.anneal(seeds, temps)
+    ref = oracle_many(oracle.OracleListing(t), seeds, temps)
+    priced = 0
+    for c, (oh, ob, oc, os_) in enumerate(ref):
+        assert np.array_equal(hist[c], oh), (name, int(seeds[c]))
+        assert np.array_equal(best[c], ob) and np.array_equal(cur[c], oc), int(seeds[c])
+        assert summ["best_energy"][c] == os_["best_energy"]
+        priced += int((oh["status"] <= 1).sum())
+    assert priced > 0 and int(summ["ambiguous"].sum()) == 0

@@ -33,10 +33,13 @@ ap.add_argument("--max-seconds", type=float, default=900)
 ap.add_argument("--verify-samples", type=int, default=10_000_000)
 ap.add_argument("--cubin", default=None,
                 help="attention cubin file in targets/ instead of the shipped one")
+ap.add_argument("--shape", default=None, help="e.g. M=512,N=512,K=2048 or B=1,H=4,S=16384 (paper shapes)")
 ap.add_argument("--out", required=True)
 a = ap.parse_args()
 
 shape = dict(B=4, H=32, S=4096) if a.target == "attn" else dict(M=4096, N=4096, K=4096)
+if a.shape:
+    shape.update({kv.split("=")[0]: int(kv.split("=")[1]) for kv in a.shape.split(",")})
 extra = {"cubin_file": a.cubin} if a.cubin else {}
 tgt = make_target(a.target, **shape, **extra).allocate()
 be = B200Backend(tgt)
@@ -70,6 +73,7 @@ out = {
     "rejected_by_screen": [{"energy": float(e), "failed": int(v.failed)} for e, v in rejected],
     "retimed_speedup": 1.0 / ratio, "retimed_speedup_iqr": [1.0 / q3, 1.0 / q1], "pairs": 45,
     "instructions_moved": int((best != be.identity).sum()),
+    "nvcc_ms": be.ref_ms, "nvcc_tflops": tgt.flops / be.ref_ms / 1e9, "cold_input_sets": be.nsets,
     "verify": {"samples": vr.samples, "passed": vr.passed, "failed": vr.failed,
                "bit_identical": vr.bitdiff_elems == 0, "seconds": round(vr.seconds, 2)},
     "trace": trace,
