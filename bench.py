@@ -59,7 +59,7 @@ def parse():
                          "sip_anneal_wave; 303 104 on a 148-SM B200)")
     ap.add_argument("--chains", type=int, default=16, help="hardware-priced chains per GPU")
     ap.add_argument("--hw-steps", type=int, default=24, help="hardware search rounds")
-    ap.add_argument("--classes", default="extended", choices=["global", "extended"],
+    ap.add_argument("--classes", default="extended", choices=["global", "extended", "sm100"],
                     help="hardware-phase candidate classes: the reference's (global) or the "
                          "sm_100 extension (DESIGN.md s5b); the simulator headline always uses global")
     ap.add_argument("--epoch", type=int, default=8, help="rounds between global-best exchanges")

@@ -69,6 +69,9 @@ typedef struct {
   const uint8_t* nrefs;   /* [n]                                            */
   const uint8_t* cut;     /* [n+1] Kernel.block_boundaries as a bitmap      */
   const uint8_t* pin;     /* [n] hardware mode: never move (may be NULL)    */
+  const uint64_t* guard;  /* [(n+1)*words] scoreboard-guard footprints of the */
+                          /* sm100 classes (tables.py); NULL = a wait mask    */
+                          /* pins its instruction (hw_safe rule 4)            */
 } sip_tables;
 
 typedef struct {

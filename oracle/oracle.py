@@ -33,7 +33,8 @@ class _Tables(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int32), ("words", ctypes.c_int32),
                 ("ctrl", ctypes.c_void_p), ("lat", ctypes.c_void_p), ("klass", ctypes.c_void_p),
                 ("reads", ctypes.c_void_p), ("writes", ctypes.c_void_p), ("refs", ctypes.c_void_p),
-                ("nrefs", ctypes.c_void_p), ("cut", ctypes.c_void_p), ("pin", ctypes.c_void_p)]
+                ("nrefs", ctypes.c_void_p), ("cut", ctypes.c_void_p), ("pin", ctypes.c_void_p),
+                ("guard", ctypes.c_void_p)]  # sm100 hardware model: unused by the oracle
 
 
 _lib = None

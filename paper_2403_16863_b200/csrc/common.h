@@ -58,6 +58,8 @@ struct KernelDev {
   uint8_t* nrefs = nullptr;
   uint8_t* cut = nullptr;       // [n+1]
   uint8_t* pin = nullptr;       // [n]
+  uint64_t* guard = nullptr;    // [(n+1)*words] sm100 scoreboard-guard footprints, or null
+  int32_t* cum = nullptr;       // [n] issue-cycle prefix sums of the listing (nvcc) order
   int16_t* gid = nullptr;       // identity -> global index (-1 = not a candidate)
   int32_t* gids = nullptr;      // global index -> identity
   uint32_t* e_after = nullptr;  // [k][nw32]  bit x = E(g, x)

@@ -45,7 +45,7 @@ class Tables(ctypes.Structure):
         ("n", ctypes.c_int32), ("words", ctypes.c_int32),
         ("ctrl", c_u32p), ("lat", c_u32p), ("klass", c_u8p),
         ("reads", c_u64p), ("writes", c_u64p), ("refs", ctypes.c_void_p),
-        ("nrefs", c_u8p), ("cut", c_u8p), ("pin", c_u8p),
+        ("nrefs", c_u8p), ("cut", c_u8p), ("pin", c_u8p), ("guard", c_u64p),
     ]
 
 
@@ -288,13 +288,16 @@ class DeviceKernel:
         self.tables = tables
         self.n = tables.n
         self._keep = [tables.ctrl, tables.lat, tables.klass, tables.reads, tables.writes,
-                      tables.refs, tables.nrefs, tables.cut, tables.pin]
+                      tables.refs, tables.nrefs, tables.cut, tables.pin, tables.guard]
+        guard = None if tables.guard is None else np.ascontiguousarray(tables.guard.reshape(-1))
+        self._keep.append(guard)
         t = Tables(
             tables.n, tables.words,
             _ptr(tables.ctrl, c_u32p), _ptr(tables.lat, c_u32p), _ptr(tables.klass, c_u8p),
             _ptr(tables.reads, c_u64p), _ptr(tables.writes, c_u64p),
             tables.refs.ctypes.data_as(ctypes.c_void_p),
             _ptr(tables.nrefs, c_u8p), _ptr(tables.cut, c_u8p), _ptr(tables.pin, c_u8p),
+            None if guard is None else _ptr(guard, c_u64p),
         )
         h = ctypes.c_void_p()
         ctx.check(ctx.lib.sip_kernel_create(ctx.handle, ctypes.byref(t), ctypes.byref(h)))
