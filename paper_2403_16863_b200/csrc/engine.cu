@@ -12,6 +12,7 @@
 // no graph is ever rebuilt.  Per-chain state layouts: Chains below.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -150,33 +151,27 @@ __host__ __device__ __forceinline__ bool c_long_r(uint32_t c) { return (c >> 25)
 // over every variable-latency instruction of the listing applies to them.  A waiting b
 // moving above a gains a wait and loses nothing: E already orders a setter before its
 // waiter and a waiter before the next setter of its barrier.
-constexpr int kGuardWords = 8;
 constexpr int kGuardScan = 1024;
 template <typename SchedAt>
 __device__ bool guard_ok(const KernelDev& d, const uint2* meta, SchedAt at, int lo, int b) {
-  if (d.words > kGuardWords) return false;
-  uint64_t tb[kGuardWords], seen[kGuardWords];
-  const uint64_t* rb = d.reads + (size_t)b * d.words;
-  const uint64_t* wb = d.writes + (size_t)b * d.words;
+  // one register word at a time (no local arrays: the scan is rare, registers are not)
   for (int w = 0; w < d.words; ++w) {
-    tb[w] = rb[w] | wb[w];
-    seen[w] = 0;
-  }
-  int p = lo - 1, steps = 0;
-  for (; p >= 0 && !d.cut[p + 1]; --p) {
-    if (++steps > kGuardScan) return false;
-    const int x = at(p);
-    const uint64_t* g = d.guard + (size_t)x * d.words;
-    if (meta[x].x & VARLAT_BIT) {
-      for (int w = 0; w < d.words; ++w)
-        if (tb[w] & g[w] & ~seen[w]) return false;
-    } else {
-      for (int w = 0; w < d.words; ++w) seen[w] |= g[w];
+    const uint64_t tb = d.reads[(size_t)b * d.words + w] | d.writes[(size_t)b * d.words + w];
+    if (tb == 0) continue;
+    uint64_t seen = 0;
+    int p = lo - 1, steps = 0;
+    for (; p >= 0 && !d.cut[p + 1]; --p) {
+      if (++steps > kGuardScan) return false;
+      const int x = at(p);
+      const uint64_t g = d.guard[(size_t)x * d.words + w];
+      if (meta[x].x & VARLAT_BIT) {
+        if (tb & g & ~seen) return false;
+      } else {
+        seen |= g;
+      }
     }
+    if (tb & d.guard[(size_t)d.n * d.words + w] & ~seen) return false;
   }
-  const uint64_t* all = d.guard + (size_t)d.n * d.words;
-  for (int w = 0; w < d.words; ++w)
-    if (tb[w] & all[w] & ~seen[w]) return false;
   return true;
 }
 
@@ -327,6 +322,10 @@ struct Chains {
                                     // them: fused chains build `best` only when it is read
                                     // (best_rows_kernel), never during the search
   int best_lazy = 0;                // 1 for fused chains: best rows are built when fetched
+  uint16_t* cid = nullptr;          // [k][C] identity in each candidate slot (SlotRow chains)
+  uint16_t* nc0 = nullptr;          // [ns] the start schedule without its candidates
+  int slots = 0;                    // 1: the last fused launch kept slots (SlotRow), its rows
+                                    // are built when read (rows_kernel)
   int64_t* replayed = nullptr;      // [C] scoreboard steps executed (instrumentation)
   int32_t* priced = nullptr;        // [C] priced iterations
 };
@@ -395,34 +394,23 @@ __device__ __forceinline__ double mt_random(ChainMt& m) {
 
 // perturb.sample_action + apply_action checks.  Returns -1 when the move is
 // legal (lo/cand/dir filled) or the SIP_ST_* rejection reason.
-template <typename Rng>
+template <typename Rng, typename Row>
 __device__ __forceinline__ int propose(const KernelDev& d, const uint2* meta, const int16_t* gid, const Chains& s,
-                                       int c, Rng& mt, int& cand, int& dir, int& lo) {
+                                       const Row& row, Rng& mt, int& cand, int& dir, int& lo, int& a, int& b) {
   uint32_t cell = mt_randbelow(mt, 2u * (uint32_t)s.k);
   cand = (int)(cell >> 1);
   dir = (int)(cell & 1u);  // 0 = UP
-  int pos = s.cpos[(size_t)cand * s.C + c];
+  int pos = row.slot_pos(cand);
   lo = dir == 0 ? pos - 1 : pos;
   if (lo < 0 || lo + 1 >= s.n) return SIP_ST_BOUNDARY;
   if (d.cut[lo + 1]) return SIP_ST_BOUNDARY;
-  const uint16_t* row = s.sched + (size_t)c * s.ns;
-  int a = row[lo], b = row[lo + 1];
+  row.pair(cand, dir, lo, a, b);
   if (!s.unsafe && edge_lookup(d, gid, a, b)) return SIP_ST_DEPENDENCY;
   if (s.hw_safe) {
-    auto at = [&](int p) { return (int)row[p]; };
+    auto at = [&](int p) { return row.at(p); };
     if (!hw_safe_ok(d, meta, at, s.n, lo, a, b, s.minfix)) return SIP_ST_HWSAFE;
   }
   return -1;
-}
-
-__device__ void apply_swap(const int16_t* gid, const Chains& s, int c, int lo, int cand, int dir) {
-  uint16_t* x = s.sched + (size_t)c * s.ns + lo;
-  uint16_t* y = x + 1;
-  uint16_t a = *x, b = *y;
-  *x = b;
-  *y = a;
-  int other = dir == 0 ? a : b;  // the neighbour the candidate traded places with
-  if (gid[other] < 0) s.cpos[(size_t)cand * s.C + c] += (dir == 0 ? -1 : 1);
 }
 
 __device__ void copy_best(const Chains& s, int c) {
@@ -659,30 +647,229 @@ __device__ __forceinline__ void replay_span(const uint2* meta, const uint16_t* r
   for (; p < p1; ++p) st.step(meta[row[p]]);
 }
 
+// ---- a chain's current schedule, two representations --------------------------
+// DenseRow: the chain-major u16 row in HBM (any number of candidates k).
+// SlotRow: with few candidates (k <= KS -- the reference's classes give both targets
+// k = 5) only the candidates' slots change: slot j (ascending position; two slots never
+// pass each other, a swap of two candidates exchanges their identities in place) sits at
+// pos(j) and holds identity id(j), in shared memory for the whole launch, and every other
+// position holds the start schedule's non-candidates in order (nc, shared memory).  A
+// replay then reads no chain state from HBM at all; the rows are materialised in HBM only
+// when read (rows_kernel).  The slot order is the candidate order perturb.candidates uses
+// (ascending positions), so `cand` indexes both the same way.
+struct DenseRow {
+  uint16_t* row;
+  uint16_t* cpos;  // s.cpos + c, stride C
+  int C;
+  __device__ __forceinline__ int at(int p) const { return row[p]; }
+  __device__ __forceinline__ int slot_pos(int j) const { return cpos[(size_t)j * C]; }
+  // identities at lo and lo + 1 of a proposal of slot `cand` (propose)
+  __device__ __forceinline__ void pair(int, int, int lo, int& a, int& b) const {
+    a = row[lo];
+    b = row[lo + 1];
+  }
+  __device__ __forceinline__ void replay(const uint2* meta, int p0, int p1, Sb& st) const {
+    replay_span(meta, row, p0, p1, st);
+  }
+  // sequential replay in pieces (ck_price, ck_restore)
+  struct Cursor {
+    int p;
+  };
+  __device__ __forceinline__ Cursor cursor(int p0) const { return Cursor{p0}; }
+  __device__ __forceinline__ void run(Cursor& u, const uint2* meta, int p1, Sb& st) const {
+    replay_span(meta, row, u.p, p1, st);
+    u.p = p1;
+  }
+  __device__ __forceinline__ void skip(Cursor& u, int p) const { u.p = p; }
+  template <typename F>
+  __device__ __forceinline__ void each(int p0, int p1, F f) const {
+    for (int p = p0; p < p1; ++p) f((int)row[p]);
+  }
+  __device__ __forceinline__ void swap(const int16_t* gid, int lo, int cand, int dir) const {
+    const uint16_t a = row[lo], b = row[lo + 1];
+    row[lo] = b;
+    row[lo + 1] = a;
+    const int other = dir == 0 ? a : b;  // the neighbour the candidate traded places with
+    if (gid[other] < 0) cpos[(size_t)cand * C] += (dir == 0 ? -1 : 1);
+  }
+  // identity at p0 + lane, the whole warp reading one row (warp_interval_lr)
+  __device__ __forceinline__ int warp_at(int p0, int lane, int n) const {
+    return p0 + lane < n ? (int)row[p0 + lane] : 0;
+  }
+  __device__ __forceinline__ DenseRow lane(int d, int ns) const {  // chain c + d's row
+    return DenseRow{row + (ptrdiff_t)d * ns, cpos + d, C};
+  }
+  // candidate positions of the start schedule (the row itself is written by the warp)
+  __device__ __forceinline__ void start(const Chains& s) const {
+    for (int j = 0; j < s.k; ++j) cpos[(size_t)j * C] = s.cpos0[j];
+  }
+  __device__ __forceinline__ void finish(const Chains&, int) const {}
+};
+__device__ __forceinline__ DenseRow dense_row(const Chains& s, int c) {
+  return DenseRow{s.sched + (size_t)c * s.ns, s.cpos + c, s.C};
+}
+
+#ifndef SIP_KS
+#define SIP_KS 8
+#endif
+constexpr int KS = SIP_KS;          // most candidate slots a SlotRow chain keeps
+constexpr int kSlotStride = 128;    // fused block size: slot columns are lane-consecutive
+struct SlotRow {
+  const uint16_t* nc;  // shared: the start schedule without its candidates
+  uint16_t* pos;       // shared: this thread's column, stride kSlotStride
+  uint16_t* id;
+  int k;
+  __device__ __forceinline__ int P(int j) const { return pos[j * kSlotStride]; }
+  __device__ __forceinline__ int I(int j) const { return id[j * kSlotStride]; }
+  __device__ __forceinline__ int at(int p) const {
+    int below = 0;
+#pragma unroll
+    for (int j = 0; j < KS; ++j) {
+      if (j >= k) break;
+      const int q = P(j);
+      if (q == p) return I(j);
+      below += q < p;
+    }
+    return nc[p - below];
+  }
+  __device__ __forceinline__ int slot_pos(int j) const { return P(j); }
+  // identities at lo and lo + 1 of a proposal of slot `cand` in O(1): exactly `cand` slots
+  // lie below its position, and its neighbour is slot cand -+ 1 or a non-candidate
+  __device__ __forceinline__ void pair(int cand, int dir, int, int& a, int& b) const {
+    const int pc = P(cand);
+    if (dir == 0) {  // (pc - 1, pc)
+      a = cand > 0 && P(cand - 1) == pc - 1 ? I(cand - 1) : (int)nc[pc - 1 - cand];
+      b = I(cand);
+    } else {  // (pc, pc + 1)
+      a = I(cand);
+      b = cand + 1 < k && P(cand + 1) == pc + 1 ? I(cand + 1) : (int)nc[pc - cand];
+    }
+  }
+  struct Cursor {
+    int p, j, q;  // next position, next slot at or after it, next non-candidate
+  };
+  __device__ __forceinline__ Cursor cursor(int p0) const {
+    int j = 0;
+    while (j < k && P(j) < p0) ++j;
+    return Cursor{p0, j, p0 - j};
+  }
+  __device__ __forceinline__ void skip(Cursor& u, int p) const {
+    while (u.j < k && P(u.j) < p) ++u.j;
+    u.p = p;
+    u.q = p - u.j;
+  }
+  __device__ __forceinline__ int next(int p, int& j, int& q) const {
+    if (j < k && P(j) == p) return I(j++);
+    return nc[q++];
+  }
+  // the same 8-aligned blocks as replay_span, so a warp's lanes step in lockstep whatever
+  // their slot layout: a block holding no slot (nearly all) gathers 8 consecutive
+  // non-candidates, one holding a slot merges them; the 8 lookups precede the updates
+  __device__ __forceinline__ void run(Cursor& u, const uint2* meta, int p1, Sb& st) const {
+    int p = u.p, j = u.j, q = u.q;
+    for (; p < p1 && (p & 7); ++p) st.step(meta[next(p, j, q)]);
+    for (; p + 8 <= p1; p += 8) {
+      uint2 m[8];
+      if (j >= k || P(j) >= p + 8) {
+#pragma unroll
+        for (int x = 0; x < 8; ++x) m[x] = meta[nc[q + x]];
+        q += 8;
+      } else {
+#pragma unroll
+        for (int x = 0; x < 8; ++x) m[x] = meta[next(p + x, j, q)];
+      }
+#pragma unroll
+      for (int x = 0; x < 8; ++x) st.step(m[x]);
+    }
+    for (; p < p1; ++p) st.step(meta[next(p, j, q)]);
+    u.p = p;
+    u.j = j;
+    u.q = q;
+  }
+  __device__ __forceinline__ void replay(const uint2* meta, int p0, int p1, Sb& st) const {
+    Cursor u = cursor(p0);
+    run(u, meta, p1, st);
+  }
+  template <typename F>
+  __device__ __forceinline__ void each(int p0, int p1, F f) const {
+    int j = 0;
+    while (j < k && P(j) < p0) ++j;
+    for (int p = p0, q = p0 - j; p < p1; ++p) {
+      if (j < k && P(j) == p) {
+        f(I(j));
+        ++j;
+      } else {
+        f((int)nc[q++]);
+      }
+    }
+  }
+  __device__ __forceinline__ void swap(const int16_t*, int lo, int cand, int dir) const {
+    (void)lo;
+    const int other = dir == 0 ? P(cand) - 1 : P(cand) + 1;
+    const int nb = dir == 0 ? cand - 1 : cand + 1;  // the neighbouring slot, if adjacent
+    if (nb >= 0 && nb < k && P(nb) == other) {
+      const uint16_t t = id[cand * kSlotStride];
+      id[cand * kSlotStride] = id[nb * kSlotStride];
+      id[nb * kSlotStride] = t;
+    } else {
+      pos[cand * kSlotStride] = (uint16_t)other;
+    }
+  }
+  // identity at p0 + lane, the whole warp reading this row: lanes 0..k-1 hold the slots,
+  // a ballot counts those below the interval and an OR-reduction marks those inside it
+  __device__ __forceinline__ int warp_at(int p0, int lane, int n) const {
+    const int sp = lane < k ? P(lane) : INT_MAX;
+    const int base = __popc(__ballot_sync(0xffffffffu, sp < p0));
+    const int off = sp - p0;
+    const uint32_t inside = __reduce_or_sync(0xffffffffu, off >= 0 && off < 32 ? 1u << off : 0u);
+    const int bt = __popc(inside & ((1u << lane) - 1u));
+    if (p0 + lane >= n) return 0;
+    return (inside >> lane) & 1u ? I(base + bt) : (int)nc[p0 + lane - base - bt];
+  }
+  __device__ __forceinline__ SlotRow lane(int d, int) const { return SlotRow{nc, pos + d, id + d, k}; }
+  __device__ __forceinline__ void start(const Chains& s) const {
+    for (int j = 0; j < k; ++j) {
+      const uint16_t p = s.cpos0[j];
+      pos[j * kSlotStride] = p;
+      id[j * kSlotStride] = s.row0[p];
+    }
+  }
+  // the final slots to HBM: rows_kernel materialises the row when it is read
+  __device__ __forceinline__ void finish(const Chains& s, int c) const {
+    for (int j = 0; j < k; ++j) {
+      s.cpos[(size_t)j * s.C + c] = (uint16_t)P(j);
+      s.cid[(size_t)j * s.C + c] = (uint16_t)I(j);
+    }
+  }
+};
+
 // total of the current schedule with (lo, lo+1) exchanged; jconv = first
 // checkpoint where the candidate rejoined the current trajectory (nck if never),
 // delta = the constant shift it rejoined with
-__device__ __forceinline__ int ck_price(const uint2* meta, const Chains& s, int c, int lo, int total_x,
-                                        int pf_x, int& jconv, int& delta, int& pf_c, int64_t& steps) {
-  const uint16_t* row = s.sched + (size_t)c * s.ns;
-  const int C = s.C, n = s.n;
+template <typename Row>
+__device__ __forceinline__ int ck_price(const uint2* meta, const Chains& s, int c, const Row& row, int lo, int a,
+                                        int b, int total_x, int pf_x, int& jconv, int& delta, int& pf_c,
+                                        int64_t& steps) {
+  const int n = s.n;
   int j0 = lo / CK;
   const OffRow off(s, c);
   Sb st;
   ck_get(s.ckpt, s, c, j0, st);
   st.shift(off.get(j0));
-  replay_span(meta, row, j0 * CK, lo, st);
-  st.step(meta[row[lo + 1]]);
+  auto cur = row.cursor(j0 * CK);
+  row.run(cur, meta, lo, st);
+  st.step(meta[b]);
   // the candidate's own states go straight into ckpt (with a zero offset): nearly every
   // priced move is accepted, and a rejected one restores them (ck_restore)
   if ((lo + 1) % CK == 0) {
     ck_put(s.ckpt, s, c, (lo + 1) / CK, st);
     off.zero((lo + 1) / CK);
   }
-  st.step(meta[row[lo]]);
+  st.step(meta[a]);
   int p = lo + 2;
+  row.skip(cur, p);
   int pb = min(n, ((p + CK - 1) / CK) * CK);
-  replay_span(meta, row, p, pb, st);
+  row.run(cur, meta, pb, st);
   steps += (pb - j0 * CK);
   delta = 0;
   const uint32_t* lrw = s.lrw + (size_t)c * s.nck4;
@@ -696,7 +883,7 @@ __device__ __forceinline__ int ck_price(const uint2* meta, const Chains& s, int 
     ck_put(s.ckpt, s, c, j, st);  // compared above; only later checkpoints are read again
     off.zero(j);
     int pe = min(n, p + CK);
-    replay_span(meta, row, p, pe, st);
+    row.run(cur, meta, pe, st);
     steps += pe - p;
   }
   jconv = s.nck;
@@ -716,14 +903,26 @@ __device__ __forceinline__ uint32_t interval_lr(const uint2* meta, const uint16_
   return L | (R << 8);
 }
 
+template <typename Row>
+__device__ __forceinline__ uint32_t interval_lr_row(const uint2* meta, const Row& row, int p0, int p1) {
+  uint32_t L = 0, R = 0;
+  row.each(p0, p1, [&](int x) {
+    const uint2 m = meta[x];
+    const uint32_t w = m.x & 63u;
+    L |= w & ~R;
+    R |= w | (m.y >> 16);
+  });
+  return L | (R << 8);
+}
+
 // After an accepted swap at (lo, lo+1) the intervals holding the pair need their L/R again
 // and the liveness W_j = L_j | (W_{j+1} & ~R_j) is carried down until it stops changing.
 // Inside one interval R_j cannot change, and L_j only for a barrier both instructions touch
 // and exactly one of them waits on (the first toucher decides whether its first event is
 // a wait); any other swap inside an interval changes nothing.
-__device__ __forceinline__ bool lr_needed(const uint2* meta, const uint16_t* row, int lo) {
+__device__ __forceinline__ bool lr_needed(const uint2* meta, int lo, int a, int b) {
   if (lo / CK != (lo + 1) / CK) return true;  // the pair straddles two intervals
-  const uint2 x = meta[row[lo]], y = meta[row[lo + 1]];
+  const uint2 x = meta[a], y = meta[b];
   const uint32_t common = ((x.x & 63u) | (x.y >> 16)) & ((y.x & 63u) | (y.y >> 16));
   return (common & (x.x ^ y.x) & 63u) != 0u;
 }
@@ -747,12 +946,14 @@ __device__ __forceinline__ void lr_store(const Chains& s, int c, int lo, uint32_
 // L | R << 8 of interval j of `row`, one position per lane (CK == 32): R is the OR of every
 // position's barriers, L the OR of the waits no earlier position touched (exclusive
 // prefix OR by shuffles).  Every lane of the (full) warp takes part.
-__device__ __forceinline__ uint32_t warp_interval_lr(const uint2* meta, const uint16_t* row, int j, int n,
+template <typename Row>
+__device__ __forceinline__ uint32_t warp_interval_lr(const uint2* meta, const Row& row, int j, int n,
                                                      int lane) {
   const int p = j * CK + lane;
+  const int x = row.warp_at(j * CK, lane, n);
   uint32_t w = 0u, t = 0u;
   if (p < n) {
-    const uint2 m = meta[row[p]];
+    const uint2 m = meta[x];
     w = m.x & 63u;
     t = w | (m.y >> 16);
   }
@@ -778,15 +979,16 @@ __device__ __forceinline__ void ck_commit(const Chains& s, int c, int lo, int jc
 
 // a rejected candidate: ck_price overwrote checkpoints in (lo / CK, jconv) with its own
 // states; replay the (unchanged) current row from the checkpoint below lo to rebuild them
-__device__ __forceinline__ int ck_restore(const uint2* meta, const Chains& s, int c, int lo, int jconv) {
-  const uint16_t* row = s.sched + (size_t)c * s.ns;
+template <typename Row>
+__device__ __forceinline__ int ck_restore(const uint2* meta, const Chains& s, int c, const Row& row, int lo, int jconv) {
   const OffRow off(s, c);
   const int j0 = lo / CK;
   Sb st;
   ck_get(s.ckpt, s, c, j0, st);
   st.shift(off.get(j0));
+  auto cur = row.cursor(j0 * CK);
   for (int j = j0 + 1; j < jconv; ++j) {
-    replay_span(meta, row, (j - 1) * CK, j * CK, st);
+    row.run(cur, meta, j * CK, st);
     ck_put(s.ckpt, s, c, j, st);
     off.zero(j);
   }
@@ -803,9 +1005,12 @@ __global__ void start_ckpt_kernel(KernelDev d, Chains s, int use_smem) {
     s.row0[p] = p < s.n ? (s.start ? s.start[p] : (uint16_t)p) : (uint16_t)0;
   __syncthreads();
   if (threadIdx.x != 0) return;
-  for (int p = 0, j = 0; p < s.n; ++p) {
+  for (int p = 0, j = 0, q = 0; p < s.n; ++p) {
     const uint16_t x = s.start ? s.start[p] : (uint16_t)p;
-    if (d.gid[x] >= 0) s.cpos0[j++] = (uint16_t)p;
+    if (d.gid[x] >= 0)
+      s.cpos0[j++] = (uint16_t)p;
+    else
+      s.nc0[q++] = x;
   }
   Sb st;
   st.reset();
@@ -834,23 +1039,56 @@ __global__ void start_ckpt_kernel(KernelDev d, Chains s, int use_smem) {
 #ifndef SIP_MINB
 #define SIP_MINB 6  // 6 resident 128-thread blocks per SM (<= 80 registers): measured best of 4-8
 #endif
-template <bool SMEM>
+// shared-memory layout of a SlotRow launch: the staged tables, then nc [ns] and the slot
+// columns pos / id [KS][kSlotStride]
+__host__ __device__ __forceinline__ size_t slots_smem_offset(int n) {
+  return (((sizeof(uint2) + sizeof(int16_t)) * (size_t)n + 15) / 16) * 16;
+}
+__host__ __device__ __forceinline__ size_t slots_smem_bytes(int n, int ns) {
+  return slots_smem_offset(n) + sizeof(uint16_t) * ((size_t)ns + 2 * KS * kSlotStride);
+}
+
+template <bool SLOTS>
+struct RowOf {
+  using T = DenseRow;
+  __device__ static T make(const Chains& s, int c, unsigned char*) { return dense_row(s, c); }
+};
+template <>
+struct RowOf<true> {
+  using T = SlotRow;
+  __device__ static T make(const Chains& s, int, unsigned char* smem) {
+    const uint16_t* nc = reinterpret_cast<const uint16_t*>(smem + slots_smem_offset(s.n));
+    uint16_t* pos = const_cast<uint16_t*>(nc) + s.ns + threadIdx.x;
+    return SlotRow{nc, pos, pos + KS * kSlotStride, s.k};
+  }
+};
+
+template <bool SMEM, bool SLOTS>
 __global__ void __launch_bounds__(128, SIP_MINB) anneal_fused_kernel(KernelDev d, Chains s,
                                                            const uint32_t* mt_base, double t0_cycles) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   Staged tb = stage_tables(d, SMEM);
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (SLOTS) {  // the start schedule's non-candidates, read by every replay
+    uint16_t* nc = reinterpret_cast<uint16_t*>(smem_raw + slots_smem_offset(s.n));
+    for (int i = threadIdx.x; i < s.n - s.k; i += blockDim.x) nc[i] = s.nc0[i];
+    __syncthreads();
+  }
   {
     // every chain starts from the same schedule: the warp writes its 32 chains' rows and
     // checkpoints cooperatively, lane-consecutive 16-byte pieces of one chain at a time,
     // so each store fills whole 128-byte lines (per-lane row writes scattered 32 rows
-    // per instruction and made initialisation a fifth of the launch)
+    // per instruction and made initialisation a fifth of the launch); SlotRow chains
+    // write no row at all
     const int lane = threadIdx.x & 31, cw = c - lane;
     const uint4* r0 = reinterpret_cast<const uint4*>(s.row0);
     const int4* k0 = reinterpret_cast<const int4*>(s.ck0);
     const int nq = s.ns / 8, nk = 2 * s.nck;
     for (int k = 0; k < 32 && cw + k < s.C; ++k) {
-      uint4* sr = reinterpret_cast<uint4*>(s.sched + (size_t)(cw + k) * s.ns);
-      for (int q = lane; q < nq; q += 32) sr[q] = r0[q];
+      if (!SLOTS) {
+        uint4* sr = reinterpret_cast<uint4*>(s.sched + (size_t)(cw + k) * s.ns);
+        for (int q = lane; q < nq; q += 32) sr[q] = r0[q];
+      }
       int4* ck = ck_at(s.ckpt, s, cw + k, 0);
       for (int q = lane; q < nk; q += 32) ck[q] = k0[q];
       int32_t* off = s.ckoff + (size_t)(cw + k) * s.offp;
@@ -864,7 +1102,8 @@ __global__ void __launch_bounds__(128, SIP_MINB) anneal_fused_kernel(KernelDev d
   const bool full_warp = CK == 32 && __ballot_sync(0xffffffffu, c < s.C) == 0xffffffffu;
   const int lane = threadIdx.x & 31;
   if (c >= s.C) return;
-  for (int j = 0; j < s.k; ++j) s.cpos[(size_t)j * s.C + c] = s.cpos0[j];
+  const typename RowOf<SLOTS>::T row = RowOf<SLOTS>::make(s, c, smem_raw);
+  row.start(s);
   ChainMt mt;  // chain-major row: a chain's draws stay in its own sectors
   mt.st = s.mt + (size_t)c * MT_N;
   {
@@ -881,27 +1120,26 @@ __global__ void __launch_bounds__(128, SIP_MINB) anneal_fused_kernel(KernelDev d
   double e_x = (double)total_x / t0, e_best = e_x;
   int best_iter = -1, amb = 0, priced = 0, nacc = 0, best_nacc = 0;
   for (int it = 0; it < s.budget; ++it) {
-    int cand, dir, lo;
-    int st = propose(d, tb.meta, tb.gid, s, c, mt, cand, dir, lo);
+    int cand, dir, lo, ia, ib;
+    int st = propose(d, tb.meta, tb.gid, s, row, mt, cand, dir, lo, ia, ib);
     double t = 0.0;
     bool lr_need = false;
     if (st < 0) {
     ++priced;
     int jconv, delta, pf_c;
-    int tc = ck_price(tb.meta, s, c, lo, total_x, pf_x, jconv, delta, pf_c, steps);
+    int tc = ck_price(tb.meta, s, c, row, lo, ia, ib, total_x, pf_x, jconv, delta, pf_c, steps);
     t = (double)tc;
     double e_c = t / t0;
     double de = e_c - e_x;
     bool acc = metropolis(de, s.temps[it], mt, amb);
     if (acc) {
-      apply_swap(tb.gid, s, c, lo, cand, dir);
+      row.swap(tb.gid, lo, cand, dir);
       ck_commit(s, c, lo, jconv, delta);
-      lr_need = lr_needed(tb.meta, s.sched + (size_t)c * s.ns, lo);
+      lr_need = lr_needed(tb.meta, lo, ia, ib);
       if (lr_need && !full_warp) {
-        const uint16_t* row = s.sched + (size_t)c * s.ns;
         const int ja = lo / CK, jb = (lo + 1) / CK;
-        lr_store(s, c, lo, interval_lr(tb.meta, row, ja * CK, min(s.n, (ja + 1) * CK)),
-                 interval_lr(tb.meta, row, jb * CK, min(s.n, (jb + 1) * CK)));
+        lr_store(s, c, lo, interval_lr_row(tb.meta, row, ja * CK, min(s.n, (ja + 1) * CK)),
+                 interval_lr_row(tb.meta, row, jb * CK, min(s.n, (jb + 1) * CK)));
       }
       pf_x = pf_c;
       __stcs(s.acclog + (size_t)nacc * s.C + c, (unsigned short)lo);
@@ -914,7 +1152,7 @@ __global__ void __launch_bounds__(128, SIP_MINB) anneal_fused_kernel(KernelDev d
         best_nacc = nacc;  // the best schedule = the current one after nacc accepted swaps
       }
     } else {
-      steps += ck_restore(tb.meta, s, c, lo, jconv);
+      steps += ck_restore(tb.meta, s, c, row, lo, jconv);
     }
     st = acc ? SIP_ST_ACCEPTED : SIP_ST_PRICED;
     }
@@ -928,7 +1166,7 @@ __global__ void __launch_bounds__(128, SIP_MINB) anneal_fused_kernel(KernelDev d
         const int L = __ffs(todo) - 1;
         todo &= todo - 1;
         const int loL = __shfl_sync(0xffffffffu, lo, L);
-        const uint16_t* rowL = s.sched + (size_t)(c - lane + L) * s.ns;
+        const auto rowL = row.lane(L - lane, s.ns);
         const uint32_t va = warp_interval_lr(tb.meta, rowL, loL / CK, s.n, lane);
         const uint32_t vb = (loL + 1) / CK != loL / CK ? warp_interval_lr(tb.meta, rowL, (loL + 1) / CK, s.n, lane) : 0u;
         if (lane == L) {
@@ -940,6 +1178,7 @@ __global__ void __launch_bounds__(128, SIP_MINB) anneal_fused_kernel(KernelDev d
     }
     record(s, c, it, st, t, lo, cand, dir);  // one (streaming) store point per iteration
   }
+  row.finish(s, c);
   s.nacc[c] = nacc;
   s.best_nacc[c] = best_iter >= 0 ? best_nacc : 0;  // no new best: the start schedule
   s.t0[c] = t0;
@@ -950,6 +1189,30 @@ __global__ void __launch_bounds__(128, SIP_MINB) anneal_fused_kernel(KernelDev d
   s.mti[c] = mt.mti == 0 ? MT_N : mt.mti;  // 624: the next draw starts a round (rng.cuh)
   s.replayed[c] = steps;
   s.priced[c] = priced;
+}
+
+// current rows of SlotRow chains [first, first + count) from their final slots and the
+// start schedule's non-candidates: one warp per chain, lane-strided positions
+__global__ void rows_kernel(Chains s, int first, int count) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= count) return;
+  const int c = first + w;
+  int P[KS], I[KS];
+#pragma unroll
+  for (int j = 0; j < KS; ++j) {
+    P[j] = j < s.k ? s.cpos[(size_t)j * s.C + c] : INT_MAX;
+    I[j] = j < s.k ? s.cid[(size_t)j * s.C + c] : 0;
+  }
+  uint16_t* row = s.sched + (size_t)c * s.ns;
+  for (int p = lane; p < s.n; p += 32) {
+    int below = 0, x = -1;
+#pragma unroll
+    for (int j = 0; j < KS; ++j) {
+      if (P[j] == p) x = I[j];
+      below += P[j] < p;
+    }
+    row[p] = (uint16_t)(x >= 0 ? x : s.nc0[p - below]);
+  }
 }
 
 // best rows of fused chains [first, first + count): the current row with the swaps accepted
@@ -997,9 +1260,10 @@ __global__ void __launch_bounds__(128) chains_propose_kernel(KernelDev d, Chains
   if (c >= s.C) return;
   MtRef mt{s.mt + (size_t)c * MT_N, 1, s.mti[c]};
   int it = s.it[c];
-  int lo = -1, cand = 0, dir = 0;
+  int lo = -1, cand = 0, dir = 0, ia, ib;
+  const DenseRow row = dense_row(s, c);
   while (it < s.budget) {
-    int st = propose(d, tb.meta, tb.gid, s, c, mt, cand, dir, lo);
+    int st = propose(d, tb.meta, tb.gid, s, row, mt, cand, dir, lo, ia, ib);
     if (st < 0) break;
     record(s, c, it, st, 0.0, lo, cand, dir);
     ++it;
@@ -1045,7 +1309,7 @@ __global__ void chains_resolve_kernel(KernelDev d, Chains s, const double* t_cur
   s.ambiguous[c] = amb;
   s.mti[c] = mt.mti;
   if (acc) {
-    apply_swap(d.gid, s, c, lo, cand, dir);
+    dense_row(s, c).swap(d.gid, lo, cand, dir);
     s.e_x[c] = e_c;
     if (de < 0 && e_c < s.e_best[c]) {
       s.e_best[c] = e_c;
@@ -1164,6 +1428,30 @@ static int configure_smem(sip_ctx* ctx, const void* fn, size_t bytes) {
 
 static constexpr size_t kSmemCap = 200 * 1024;
 
+// The fused launch variant for a listing: SlotRow chains when the candidates are few
+// (k <= KS) and nc plus the slot columns fit beside the staged tables; else dense rows
+// (tables staged when they fit).  `bytes` = dynamic shared memory per block.
+enum class Fused { kDenseGlobal, kDenseSmem, kSlots };
+static Fused fused_variant(const KernelDev& d, size_t* bytes) {
+  const int ns = (d.n + 7) & ~7;
+  const size_t slots = slots_smem_bytes(d.n, ns);
+  if (d.k > 0 && d.k <= KS && slots <= kSmemCap && !getenv("SIP_NO_SLOTS")) {
+    *bytes = slots;
+    return Fused::kSlots;
+  }
+  *bytes = smem_need(d);
+  if (*bytes <= kSmemCap) return Fused::kDenseSmem;
+  *bytes = 0;
+  return Fused::kDenseGlobal;
+}
+static const void* fused_fn(Fused v) {
+  switch (v) {
+    case Fused::kSlots: return (const void*)anneal_fused_kernel<true, true>;
+    case Fused::kDenseSmem: return (const void*)anneal_fused_kernel<true, false>;
+    default: return (const void*)anneal_fused_kernel<false, false>;
+  }
+}
+
 }  // namespace sip
 
 using namespace sip;
@@ -1225,6 +1513,8 @@ static int chains_alloc(sip_ctx* ctx, sip_kernel* k, const sip_anneal_cfg* cfg, 
   TRY(dalloc(ctx, &s.lrw0, (size_t)s.nck4));
   TRY(dalloc(ctx, &s.row0, (size_t)s.ns));
   TRY(dalloc(ctx, &s.cpos0, (size_t)std::max(s.k, 1)));
+  TRY(dalloc(ctx, &s.cid, (size_t)std::max(s.k, 1) * C));
+  TRY(dalloc(ctx, &s.nc0, (size_t)s.ns));
   TRY(dalloc(ctx, &s.acclog, (size_t)std::max(s.budget, 1) * C));
   TRY(dalloc(ctx, &s.nacc, C));
   TRY(dalloc(ctx, &s.best_nacc, C));
@@ -1248,7 +1538,7 @@ static void chains_free(sip_chains* o) {
   void* ptrs[] = {s.sched, s.best, s.cpos, s.mt, s.mti, s.t0, s.e_x, s.e_best, s.it,
                   s.best_iter, s.ambiguous, s.p_lo, s.p_cand, s.p_dir, s.hist, o->d_temps,
                   o->d_seeds, o->d_tcurr, o->d_status, o->d_lo, s.cand_out, o->d_adopt,
-                  s.ckpt, s.ckoff, s.ck0, s.lrw, s.lrw0, s.row0, s.cpos0, s.acclog, s.nacc, s.best_nacc, s.replayed, s.priced, o->d_start,
+                  s.ckpt, s.ckoff, s.ck0, s.lrw, s.lrw0, s.row0, s.cpos0, s.cid, s.nc0, s.acclog, s.nacc, s.best_nacc, s.replayed, s.priced, o->d_start,
                   o->d_summary};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -1289,9 +1579,18 @@ __global__ void pack_summary_kernel(Chains s, sip_chain_summary* out) {
                              s.replayed ? s.replayed[c] : 0, s.priced ? s.priced[c] : 0, 0};
 }
 
+// SlotRow chains keep no row during the search: build the current rows of [first, first + count)
+static int ensure_rows(sip_ctx* ctx, const Chains& s, int first, int count) {
+  if (!s.slots || count <= 0) return SIP_OK;
+  rows_kernel<<<(count + 3) / 4, 128, 0, ctx->stream>>>(s, first, count);
+  SIP_CHECK_LAUNCH(ctx);
+  return SIP_OK;
+}
+
 // fused chains keep no best rows during the search: build those of [first, first + count)
 static int ensure_best(sip_ctx* ctx, const Chains& s, int first, int count) {
   if (!s.best_lazy || count <= 0) return SIP_OK;
+  TRY(ensure_rows(ctx, s, first, count));
   best_rows_kernel<<<(count + 3) / 4, 128, 0, ctx->stream>>>(s, first, count);
   SIP_CHECK_LAUNCH(ctx);
   return SIP_OK;
@@ -1305,6 +1604,7 @@ static int chains_fetch(sip_chains* o, sip_record* history, uint16_t* best, uint
   if (history) TRY(fetch_history(ctx, s, 0, (int)C, history));
   if (best) TRY(ensure_best(ctx, s, 0, s.C));
   if (best) TRY(fetch_sched(ctx, s.best, s.n, s.ns, s.C, best));
+  if (current) TRY(ensure_rows(ctx, s, 0, s.C));
   if (current) TRY(fetch_sched(ctx, s.sched, s.n, s.ns, s.C, current));
   if (summary) {  // packed on the device, one copy
     if (!o->d_summary) TRY(dalloc(ctx, &o->d_summary, C));
@@ -1575,17 +1875,19 @@ static int run_fused(sip_kernel* k, const sip_anneal_cfg* cfg, const int64_t* se
   }
   size_t sm = smem_need(k->d);
   int use_smem = sm <= kSmemCap;
-  if (use_smem) {
-    TRY(configure_smem(ctx, (const void*)anneal_fused_kernel<true>, sm));
-    TRY(configure_smem(ctx, (const void*)start_ckpt_kernel, sm));
-  }
+  if (use_smem) TRY(configure_smem(ctx, (const void*)start_ckpt_kernel, sm));
   start_ckpt_kernel<<<1, 128, use_smem ? sm : 0, ctx->stream>>>(k->d, o.s, use_smem);
-  if (use_smem)
-    anneal_fused_kernel<true><<<(chains + 127) / 128, 128, sm, ctx->stream>>>(k->d, o.s, k->d_base,
-                                                                             (double)k->baseline);
+  size_t fsm = 0;
+  const Fused v = fused_variant(k->d, &fsm);
+  o.s.slots = v == Fused::kSlots ? 1 : 0;
+  if (fsm) TRY(configure_smem(ctx, fused_fn(v), fsm));
+  const int grid = (chains + 127) / 128;
+  if (v == Fused::kSlots)
+    anneal_fused_kernel<true, true><<<grid, 128, fsm, ctx->stream>>>(k->d, o.s, k->d_base, (double)k->baseline);
+  else if (v == Fused::kDenseSmem)
+    anneal_fused_kernel<true, false><<<grid, 128, fsm, ctx->stream>>>(k->d, o.s, k->d_base, (double)k->baseline);
   else
-    anneal_fused_kernel<false><<<(chains + 127) / 128, 128, 0, ctx->stream>>>(k->d, o.s, k->d_base,
-                                                                              (double)k->baseline);
+    anneal_fused_kernel<false, false><<<grid, 128, 0, ctx->stream>>>(k->d, o.s, k->d_base, (double)k->baseline);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ctx, SIP_E_CUDA, std::string("anneal: ") + cudaGetErrorString(e));
   return SIP_OK;
@@ -1867,6 +2169,7 @@ int sip_results_fetch(sip_results* r, int32_t first, int32_t count, sip_record* 
   if (history) TRY(fetch_history(ctx, s, first, count, history));
   if (best) TRY(ensure_best(ctx, s, first, count));
   if (best) TRY(fetch_sched(ctx, s.best + (size_t)first * s.ns, s.n, s.ns, count, best));
+  if (current) TRY(ensure_rows(ctx, s, first, count));
   if (current) TRY(fetch_sched(ctx, s.sched + (size_t)first * s.ns, s.n, s.ns, count, current));
   SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return SIP_OK;
@@ -1890,14 +2193,11 @@ int sip_anneal_wave(sip_kernel* k, int32_t* chains) {
   if (!k || !chains) return SIP_E_ARG;
   sip_ctx* ctx = k->ctx;
   SIP_CUDA(ctx, cudaSetDevice(ctx->device));
-  size_t sm = smem_need(k->d);
-  int use_smem = sm <= kSmemCap;
-  if (use_smem) TRY(configure_smem(ctx, (const void*)anneal_fused_kernel<true>, sm));
+  size_t fsm = 0;
+  const Fused v = fused_variant(k->d, &fsm);
+  if (fsm) TRY(configure_smem(ctx, fused_fn(v), fsm));
   int per_sm = 0;
-  if (use_smem)
-    SIP_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, anneal_fused_kernel<true>, 128, sm));
-  else
-    SIP_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, anneal_fused_kernel<false>, 128, 0));
+  SIP_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_fn(v), 128, fsm));
   *chains = per_sm * ctx->sm_count * 128;
   return SIP_OK;
 }
