@@ -681,6 +681,13 @@ struct DenseRow {
     u.p = p1;
   }
   __device__ __forceinline__ void skip(Cursor& u, int p) const { u.p = p; }
+  // the 8 identities of the aligned block at u.p (one 16-byte load; rows are zero-padded)
+  __device__ __forceinline__ void gather8(Cursor& u, int x[8]) const {
+    const uint4 v = *reinterpret_cast<const uint4*>(row + u.p);
+    x[0] = v.x & 0xffffu; x[1] = v.x >> 16; x[2] = v.y & 0xffffu; x[3] = v.y >> 16;
+    x[4] = v.z & 0xffffu; x[5] = v.z >> 16; x[6] = v.w & 0xffffu; x[7] = v.w >> 16;
+    u.p += 8;
+  }
   template <typename F>
   __device__ __forceinline__ void each(int p0, int p1, F f) const {
     for (int p = p0; p < p1; ++p) f((int)row[p]);
@@ -762,25 +769,39 @@ struct SlotRow {
     if (j < k && P(j) == p) return I(j++);
     return nc[q++];
   }
+  // the 8 identities of the aligned block at u.p: a block holding no slot (nearly all)
+  // gathers 8 consecutive non-candidates, one holding a slot merges them.  Positions past
+  // the listing's end read the zero padding that follows nc (never stepped).
+  __device__ __forceinline__ void gather8(Cursor& u, int x[8]) const {
+    const int p = u.p;
+    if (u.j >= k || P(u.j) >= p + 8) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) x[t] = nc[u.q + t];
+      u.q += 8;
+    } else {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) x[t] = next(p + t, u.j, u.q);
+    }
+    u.p = p + 8;
+  }
   // the same 8-aligned blocks as replay_span, so a warp's lanes step in lockstep whatever
-  // their slot layout: a block holding no slot (nearly all) gathers 8 consecutive
-  // non-candidates, one holding a slot merges them; the 8 lookups precede the updates
+  // their slot layout; the 8 lookups precede the updates
   __device__ __forceinline__ void run(Cursor& u, const uint2* meta, int p1, Sb& st) const {
     int p = u.p, j = u.j, q = u.q;
     for (; p < p1 && (p & 7); ++p) st.step(meta[next(p, j, q)]);
-    for (; p + 8 <= p1; p += 8) {
+    u.p = p;
+    u.j = j;
+    u.q = q;
+    for (; u.p + 8 <= p1;) {
+      int x[8];
+      gather8(u, x);
       uint2 m[8];
-      if (j >= k || P(j) >= p + 8) {
 #pragma unroll
-        for (int x = 0; x < 8; ++x) m[x] = meta[nc[q + x]];
-        q += 8;
-      } else {
+      for (int t = 0; t < 8; ++t) m[t] = meta[x[t]];
 #pragma unroll
-        for (int x = 0; x < 8; ++x) m[x] = meta[next(p + x, j, q)];
-      }
-#pragma unroll
-      for (int x = 0; x < 8; ++x) st.step(m[x]);
+      for (int t = 0; t < 8; ++t) st.step(m[t]);
     }
+    p = u.p, j = u.j, q = u.q;
     for (; p < p1; ++p) st.step(meta[next(p, j, q)]);
     u.p = p;
     u.j = j;
@@ -856,20 +877,36 @@ __device__ __forceinline__ int ck_price(const uint2* meta, const Chains& s, int 
   Sb st;
   ck_get(s.ckpt, s, c, j0, st);
   st.shift(off.get(j0));
+  // aligned blocks of 8 from the checkpoint to the first checkpoint boundary past the
+  // pair, with the pair's identities exchanged in the block(s) holding it: every lane of
+  // a warp runs the same block code (no head or tail loops around lo)
   auto cur = row.cursor(j0 * CK);
-  row.run(cur, meta, lo, st);
-  st.step(meta[b]);
-  // the candidate's own states go straight into ckpt (with a zero offset): nearly every
-  // priced move is accepted, and a rejected one restores them (ck_restore)
-  if ((lo + 1) % CK == 0) {
-    ck_put(s.ckpt, s, c, (lo + 1) / CK, st);
-    off.zero((lo + 1) / CK);
+  int p = j0 * CK;
+  const int pb = min(n, ((lo + 2 + CK - 1) / CK) * CK);
+  for (; p < pb; p += 8) {
+    if (p == lo + 1 && p % CK == 0) {
+      // the candidate's own states go straight into ckpt (with a zero offset): nearly every
+      // priced move is accepted, and a rejected one restores them (ck_restore)
+      ck_put(s.ckpt, s, c, p / CK, st);
+      off.zero(p / CK);
+    }
+    int x[8];
+    row.gather8(cur, x);
+    if (p <= lo + 1 && lo < p + 8) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) x[t] = p + t == lo ? b : p + t == lo + 1 ? a : x[t];
+    }
+    uint2 m[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) m[t] = meta[x[t]];
+    const int cnt = min(8, n - p);
+    if (cnt == 8) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) st.step(m[t]);
+    } else {
+      for (int t = 0; t < cnt; ++t) st.step(m[t]);
+    }
   }
-  st.step(meta[a]);
-  int p = lo + 2;
-  row.skip(cur, p);
-  int pb = min(n, ((p + CK - 1) / CK) * CK);
-  row.run(cur, meta, pb, st);
   steps += (pb - j0 * CK);
   delta = 0;
   const uint32_t* lrw = s.lrw + (size_t)c * s.nck4;
@@ -1039,6 +1076,9 @@ __global__ void start_ckpt_kernel(KernelDev d, Chains s, int use_smem) {
 #ifndef SIP_MINB
 #define SIP_MINB 6  // 6 resident 128-thread blocks per SM (<= 80 registers): measured best of 4-8
 #endif
+#ifndef SIP_MINB_SLOTS
+#define SIP_MINB_SLOTS 7  // SlotRow chains keep no row in HBM: 7 blocks (<= 72 registers)
+#endif
 // shared-memory layout of a SlotRow launch: the staged tables, then nc [ns] and the slot
 // columns pos / id [KS][kSlotStride]
 __host__ __device__ __forceinline__ size_t slots_smem_offset(int n) {
@@ -1064,14 +1104,14 @@ struct RowOf<true> {
 };
 
 template <bool SMEM, bool SLOTS>
-__global__ void __launch_bounds__(128, SIP_MINB) anneal_fused_kernel(KernelDev d, Chains s,
+__global__ void __launch_bounds__(128, SLOTS ? SIP_MINB_SLOTS : SIP_MINB) anneal_fused_kernel(KernelDev d, Chains s,
                                                            const uint32_t* mt_base, double t0_cycles) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Staged tb = stage_tables(d, SMEM);
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (SLOTS) {  // the start schedule's non-candidates, read by every replay
     uint16_t* nc = reinterpret_cast<uint16_t*>(smem_raw + slots_smem_offset(s.n));
-    for (int i = threadIdx.x; i < s.n - s.k; i += blockDim.x) nc[i] = s.nc0[i];
+    for (int i = threadIdx.x; i < s.ns; i += blockDim.x) nc[i] = i < s.n - s.k ? s.nc0[i] : (uint16_t)0;
     __syncthreads();
   }
   {
