@@ -2220,7 +2220,11 @@ int sip_anneal_state_bytes(sip_kernel* k, int32_t budget, int64_t* per_chain) {
   const int64_t n = k->d.n, ns = (n + 7) & ~7, kk = std::max(k->d.k, 1), B = std::max(budget, 1);
   const int64_t nck = (n + CK - 1) / CK, nck4 = (nck + 3) & ~3, nck8 = (nck + 7) & ~7;
   const int64_t offp = nck8 + ((((nck + 7) >> 3) + 3) & ~3);
-  *per_chain = 2 * ns * 2                 // sched, best
+  // SlotRow chains (k <= KS) work on their slots and never touch the rows during a launch
+  // (rows are built when read); dense chains work on the current row
+  size_t fsm = 0;
+  const bool slots = fused_variant(k->d, &fsm) == Fused::kSlots;
+  *per_chain = (slots ? 2 * 2 * kk : 2 * ns * 2)  // slots (position, identity) or sched + best
                + 4 * (int64_t)MT_N        // MT words
                + 2 * kk                   // candidate positions
                + 32 * nck + 4 * offp + 4 * nck4  // checkpoints, offsets, interval masks

@@ -11,4 +11,4 @@ import json,sys; d=json.loads([l for l in sys.stdin if l.startswith('{')][-1]); 
 done; done
 unset SIP_NO_SLOTS
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:anneal_fused -s 1 -c 1 \
-  -o gpurun_out/engine_${TAG} python tools/profile_kernels.py engine 227328 > gpurun_out/${TAG}_ncu.log 2>&1
+  -o gpurun_out/engine_${TAG} python tools/profile_kernels.py engine 265216 > gpurun_out/${TAG}_ncu.log 2>&1
