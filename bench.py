@@ -506,6 +506,9 @@ def library_tflops(kind, tgt, reps: int = 15) -> dict:
     return {"tflops": tgt.flops / ms / 1e9, "ms": ms, "what": name}
 
 
+FULL_SHAPE_INPUTS = 16  # independent Philox input sets compared at the tuned shape
+
+
 def hardware_phase(kind, listing, local, rank, world, dist, args, rounds, shape=None):
     """Hardware-priced search on one tuning target: rate, roofline, tuned vs nvcc, verification."""
     import numpy as np
@@ -637,6 +640,14 @@ def hardware_phase(kind, listing, local, rank, world, dist, args, rounds, shape=
                              else "one independent head, S=512 D=128") + ", Philox inputs; baseline "
                             "and champion launched on it, outputs compared (sip_compare)",
                   "tolerance": {"atol": ver.atol, "rtol": ver.rtol}}
+        # the same comparison at the tuned shape itself (one sample = one full problem of the
+        # benchmarked size), so the accepted schedule is checked where it was timed too
+        full = Verifier(kind, device=local, batch=1, shape=dict(shape))
+        vf = full.run(best, FULL_SHAPE_INPUTS, check_every=FULL_SHAPE_INPUTS)
+        verify["tuned_shape"] = {"inputs": vf.samples, "passed": vf.passed, "failed": vf.failed,
+                                 "bit_identical": vf.bitdiff_elems == 0, "shape": dict(shape),
+                                 "seconds": vf.seconds}
+        del full
     return {"roofline": roofline, "hw": hw, "tuned": tuned, "verify": verify, "launches": h_launch}
 
 
@@ -702,7 +713,11 @@ def main() -> None:
     dk = ctx.kernel(tables)
     acfg = AnnealConfig()  # reference defaults: T 1.0 -> 0.01, cooling 1.05, 95 iterations
     temps = acfg.temperatures()
-    C = args.sim_chains or 2 * dk.wave_chains()  # whole waves: no partially filled last wave
+    # 12 blocks of 128 chains per SM (two waves at the dense kernel's 6 resident blocks, 1.7 at
+    # SlotRow's 7): measured best for the public-API (e2e) rate, chains from the nvcc schedule
+    # -- 2 full SlotRow waves (265 216 chains) gave 3.82e9 engine but 2.84e9 e2e, 227 328 gave
+    # 3.72e9 / 3.24e9, 132 608 3.50e9 / 3.05e9
+    C = args.sim_chains or 12 * 128 * ctx.sm_count
     best = {"e": 1.0, "perm": None}
 
     def epoch(ep: int):
