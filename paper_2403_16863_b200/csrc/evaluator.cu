@@ -18,6 +18,7 @@
 #include <cstring>
 #include <list>
 #include <string>
+#include <chrono>
 #include <thread>
 #include <unordered_map>
 #include <vector>
@@ -821,8 +822,12 @@ static int measure_round_impl(sip_module* m, const uint16_t* perm_ref, const uin
   sip_ctx* ctx = m->ctx;
   CachedMod* ref = nullptr;
   std::vector<CachedMod*> mods;
+  static const bool timing = getenv("SIP_EVAL_TIMING") != nullptr;
+  const auto now = [] { return std::chrono::steady_clock::now(); };
+  const auto t_begin = now();
   int rc = load_batch(m, perm_ref, perms, k, &ref, mods, status);
   if (rc != SIP_OK) return rc;
+  const auto t_loaded = now();
   if (flush_l2 && (rc = ensure_flush(ctx)) != SIP_OK) return rc;
   // the round's modules: slot 0 = the reference, then the loadable candidates
   std::vector<CachedMod*> set{ref};
@@ -861,9 +866,16 @@ static int measure_round_impl(sip_module* m, const uint16_t* perm_ref, const uin
     return rc;
   }
   if (ce != cudaSuccess) return sip::fail(ctx, SIP_E_MEASURE, std::string("capture: ") + cudaGetErrorString(ce));
+  const auto t_captured = now();
   ce = cudaGraphInstantiate(&exec, graph, 0);
+  const auto t_inst = now();
   if (ce == cudaSuccess) ce = cudaGraphLaunch(exec, ctx->stream);
   if (ce == cudaSuccess) ce = cudaStreamSynchronize(ctx->stream);
+  if (timing) {
+    const auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    fprintf(stderr, "[sip round] k=%d load %.3f capture %.3f instantiate %.3f execute %.3f ms\n", k,
+            ms(t_begin, t_loaded), ms(t_loaded, t_captured), ms(t_captured, t_inst), ms(t_inst, now()));
+  }
   std::vector<double> tref(reps);
   for (int r = 0; r < reps && ce == cudaSuccess; ++r) {
     float a = 0.f;
