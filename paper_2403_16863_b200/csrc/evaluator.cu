@@ -15,6 +15,8 @@
 #include <elf.h>
 
 #include <algorithm>
+#include <atomic>
+#include <memory>
 #include <cstring>
 #include <list>
 #include <string>
@@ -644,6 +646,10 @@ static int measure_round_impl(sip_module* m, const uint16_t* perm_ref, const uin
                               const sip_launch* L, int32_t nL, int32_t warmup, int32_t reps, int32_t flush_l2,
                               double* ratio_median, double* ref_median_ms, double* cand_median_ms,
                               double* raw_ratio, int32_t* status);
+static int measure_round_streamed(sip_module* m, const uint16_t* perm_ref, const uint16_t* perms, int32_t k,
+                                  const sip_launch* L, int32_t nL, int32_t warmup, int32_t reps,
+                                  int32_t flush_l2, double* ratio_median, double* ref_median_ms,
+                                  double* cand_median_ms, double* raw_ratio, int32_t* status);
 
 int sip_measure_round(sip_module* m, const uint16_t* perm_ref, const uint16_t* perms, int32_t k,
                       const sip_launch* L, int32_t nL, int32_t warmup, int32_t reps, int32_t flush_l2,
@@ -651,8 +657,11 @@ int sip_measure_round(sip_module* m, const uint16_t* perm_ref, const uint16_t* p
                       double* raw_ratio, int32_t* status) {
   if (!m || !L || nL < 1 || !m->ctx || !perms || k < 1 || !ratio_median || !status || reps < 1 || warmup < 0)
     return SIP_E_ARG;
-  const int rc = measure_round_impl(m, perm_ref, perms, k, L, nL, warmup, reps, flush_l2, ratio_median,
-                                    ref_median_ms, cand_median_ms, raw_ratio, status);
+  static const bool graph = getenv("SIP_ROUND_GRAPH") != nullptr;  // the captured-graph round (A/B)
+  const int rc = graph ? measure_round_impl(m, perm_ref, perms, k, L, nL, warmup, reps, flush_l2, ratio_median,
+                                            ref_median_ms, cand_median_ms, raw_ratio, status)
+                       : measure_round_streamed(m, perm_ref, perms, k, L, nL, warmup, reps, flush_l2,
+                                                ratio_median, ref_median_ms, cand_median_ms, raw_ratio, status);
   for (auto& c : m->cache) c.pinned = false;
   return rc;
 }
@@ -899,6 +908,166 @@ static int measure_round_impl(sip_module* m, const uint16_t* perm_ref, const uin
   }
   if (exec) cudaGraphExecDestroy(exec);
   cudaGraphDestroy(graph);
+  if (ce != cudaSuccess)
+    return sip::fail(ctx, SIP_E_MEASURE, std::string("timed launches: ") + cudaGetErrorString(ce));
+  return SIP_OK;
+}
+
+// The streamed round (the default): the candidates' modules load on worker threads while the
+// device already runs the reference's warm-up launches and those of every candidate loaded so
+// far, so module loading hides behind warm-up work instead of preceding the whole round; the
+// timed launches then go straight onto the stream between event pairs (the host enqueues the
+// round's ~100 launches in far less time than the first one runs, so they execute back to
+// back as in a captured graph, without the capture and instantiation).  Same launch order,
+// input-set rotation and median-of-ratios semantics as measure_round_impl.
+static int measure_round_streamed(sip_module* m, const uint16_t* perm_ref, const uint16_t* perms, int32_t k,
+                                  const sip_launch* L, int32_t nL, int32_t warmup, int32_t reps,
+                                  int32_t flush_l2, double* ratio_median, double* ref_median_ms,
+                                  double* cand_median_ms, double* raw_ratio, int32_t* status) {
+  sip_ctx* ctx = m->ctx;
+  static const bool timing = getenv("SIP_EVAL_TIMING") != nullptr;
+  const auto now = [] { return std::chrono::steady_clock::now(); };
+  const auto t_begin = now();
+  if (m->cache_cap < (size_t)k + 1) m->cache_cap = (size_t)k + 1;
+  CachedMod* ref = nullptr;
+  int rc = get_module(m, perm_ref, &ref);
+  if (rc != SIP_OK) return rc;
+  ref->pinned = true;
+  std::vector<CachedMod*> mods(k, nullptr);
+  std::vector<int> todo;
+  for (int i = 0; i < k; ++i) {
+    const uint16_t* p = perms + (size_t)i * m->n;
+    std::vector<uint16_t> key(p, p + m->n);
+    if (CachedMod* hit = find_module(m, key)) {
+      hit->pinned = true;
+      mods[i] = hit;
+    }
+    status[i] = SIP_OK;
+    if (!mods[i]) todo.push_back(i);
+  }
+  const size_t nt = todo.size();
+  std::vector<std::vector<uint8_t>> imgs(nt);
+  std::vector<CUmodule> loaded(nt, nullptr);
+  std::vector<CUfunction> fns(nt, nullptr);
+  std::unique_ptr<std::atomic<int>[]> ready(new std::atomic<int>[nt > 0 ? nt : 1]);
+  for (size_t t = 0; t < nt; ++t) {
+    ready[t].store(0);
+    if (build_image(m, perms + (size_t)todo[t] * m->n, imgs[t]) != SIP_OK) ready[t].store(-1);
+  }
+  CUcontext cur = nullptr;
+  if (ctx->cuCtxGetCurrent(&cur) != CUDA_SUCCESS || cur == nullptr) {
+    SIP_CUDA(ctx, cudaFree(nullptr));
+    ctx->cuCtxGetCurrent(&cur);
+  }
+  const char* lt = getenv("SIP_LOAD_THREADS");
+  const int want = lt ? std::max(1, atoi(lt)) : 8;
+  const int nthreads = (int)std::min<size_t>(nt, (size_t)want);
+  std::vector<std::thread> pool;
+  for (int w = 0; w < nthreads; ++w)
+    pool.emplace_back([&, w]() {
+      const bool ctx_ok = ctx->cuCtxSetCurrent(cur) == CUDA_SUCCESS;
+      for (size_t t = w; t < nt; t += nthreads) {
+        if (ready[t].load() != 0) continue;  // image could not be built
+        bool ok = ctx_ok && ctx->cuModuleLoadData(&loaded[t], imgs[t].data()) == CUDA_SUCCESS;
+        if (ok && ctx->cuModuleGetFunction(&fns[t], loaded[t], m->func.c_str()) != CUDA_SUCCESS) {
+          ctx->cuModuleUnload(loaded[t]);
+          loaded[t] = nullptr;
+          ok = false;
+        }
+        ready[t].store(ok ? 1 : -1, std::memory_order_release);
+      }
+    });
+  auto join = [&]() {
+    for (auto& th : pool)
+      if (th.joinable()) th.join();
+  };
+  if (flush_l2 && (rc = ensure_flush(ctx)) != SIP_OK) {
+    join();
+    return rc;
+  }
+  int slot = 0;
+  for (int w = 0; w < warmup && rc == SIP_OK; ++w) rc = launch(m, ref, &L[slot++ % nL]);
+  // warm-ups in candidate order, each as soon as its module is there
+  size_t t = 0;
+  for (int i = 0; i < k && rc == SIP_OK; ++i) {
+    if (!mods[i]) {  // the next module being loaded (todo is ascending)
+      int st;
+      while ((st = ready[t].load(std::memory_order_acquire)) == 0) std::this_thread::yield();
+      if (st < 0) {
+        status[i] = SIP_E_MEASURE;
+        ++t;
+        continue;
+      }
+      CachedMod cm;
+      cm.perm.assign(perms + (size_t)i * m->n, perms + (size_t)(i + 1) * m->n);
+      cm.mod = loaded[t];
+      cm.fn = fns[t];
+      cm.stamp = ++m->clock;
+      cm.pinned = true;
+      if (m->cache.size() >= m->cache_cap) evict_one(m);
+      mods[i] = insert_module(m, std::move(cm));
+      ++t;
+    }
+    for (int w = 0; w < warmup && rc == SIP_OK; ++w) rc = launch(m, mods[i], &L[slot++ % nL]);
+  }
+  join();
+  // modules a failed launch left unclaimed still belong to the cache-less tail: unload them
+  for (size_t u = t; u < nt; ++u)
+    if (ready[u].load() > 0) ctx->cuModuleUnload(loaded[u]);
+  if (rc != SIP_OK) return rc;
+  const auto t_warm = now();
+  std::vector<CachedMod*> set{ref};
+  std::vector<int> cand_of{-1};
+  for (int i = 0; i < k; ++i)
+    if (status[i] == SIP_OK) {
+      set.push_back(mods[i]);
+      cand_of.push_back(i);
+    }
+  const int nm = (int)set.size();
+  const int nev = 2 * reps * nm;
+  while ((int)m->events.size() < nev) {
+    cudaEvent_t e;
+    SIP_CUDA(ctx, cudaEventCreate(&e));
+    m->events.push_back(e);
+  }
+  for (int r = 0; r < reps && rc == SIP_OK; ++r)
+    for (int q = 0; q < nm && rc == SIP_OK; ++q) {
+      const int j = (q + r) % nm;  // rotate the order every rep
+      const int e = 2 * (r * nm + j);
+      if (flush_l2) cudaMemsetAsync(ctx->flush_buf, (r * nm + q) & 0xff, ctx->flush_bytes, ctx->stream);
+      cudaEventRecord(m->events[e], ctx->stream);
+      rc = launch(m, set[j], &L[slot++ % nL]);
+      cudaEventRecord(m->events[e + 1], ctx->stream);
+    }
+  if (rc != SIP_OK) return rc;
+  const auto t_enq = now();
+  cudaError_t ce = cudaStreamSynchronize(ctx->stream);
+  if (timing)
+    fprintf(stderr, "[sip round streamed] k=%d load+warmup-enqueue %.3f timed-enqueue %.3f execute %.3f ms\n", k,
+            std::chrono::duration<double, std::milli>(t_warm - t_begin).count(),
+            std::chrono::duration<double, std::milli>(t_enq - t_warm).count(),
+            std::chrono::duration<double, std::milli>(now() - t_enq).count());
+  std::vector<double> tref(reps);
+  for (int r = 0; r < reps && ce == cudaSuccess; ++r) {
+    float a = 0.f;
+    ce = cudaEventElapsedTime(&a, m->events[2 * r * nm], m->events[2 * r * nm + 1]);
+    tref[r] = a;
+  }
+  for (int q = 1; q < nm && ce == cudaSuccess; ++q) {
+    const int i = cand_of[q];
+    std::vector<double> tc(reps), ratio(reps);
+    for (int r = 0; r < reps && ce == cudaSuccess; ++r) {
+      float b = 0.f;
+      const int e = 2 * (r * nm + q);
+      ce = cudaEventElapsedTime(&b, m->events[e], m->events[e + 1]);
+      tc[r] = b;
+      ratio[r] = b / tref[r];
+    }
+    ratio_median[i] = median_of(ratio);
+    if (ref_median_ms) ref_median_ms[i] = median_of(tref);
+    if (cand_median_ms) cand_median_ms[i] = median_of(tc);
+    if (raw_ratio) std::copy(ratio.begin(), ratio.end(), raw_ratio + (size_t)i * reps);
+  }
   if (ce != cudaSuccess)
     return sip::fail(ctx, SIP_E_MEASURE, std::string("timed launches: ") + cudaGetErrorString(ce));
   return SIP_OK;
