@@ -381,6 +381,69 @@ struct ChainMt {
     return v;
   }
 };
+// The same generator with its row read and written two words at a time (8-byte accesses
+// at even word indices: half the L1/L2 requests).  Every round of draws starts at word 0,
+// so draw i is even on every second call: an even draw loads the pair holding word i+2
+// (its partner i+3 is held for the draw after) and the pair holding word i+398, and an
+// odd draw stores the regenerated pair (i-1, i).  No draw reads a word stored later than
+// 225 draws before it, so the delayed store is invisible; finish() stores a pending word.
+struct ChainMt2 {
+  uint32_t* st;
+  int mti;                // index of the next draw
+  uint32_t a, b, j;       // its operands: words i, i+1, i+397
+  uint32_t ha, hb, hv;    // held: word i+2 (odd i), word i+398 (odd i), regenerated word i-1 (odd i)
+  __device__ __forceinline__ uint2 pair(int w) const {  // w even
+    return *reinterpret_cast<const uint2*>(st + w);
+  }
+  __device__ __forceinline__ void load(int i) {  // i even (a round starts at word 0)
+    const uint2 p0 = pair(i);
+    a = p0.x;
+    b = p0.y;
+    const int k = i + MT_M - 1 < MT_N ? i + MT_M - 1 : i + MT_M - 1 - MT_N;  // even: pair (i+396, i+397)
+    j = pair(k).y;
+  }
+  __device__ __forceinline__ uint32_t next() {
+    const int i = mti;
+    const uint32_t y = (a & 0x80000000u) | (b & 0x7fffffffu);
+    uint32_t v = j ^ (y >> 1) ^ ((y & 1u) ? 0x9908b0dfu : 0u);
+    const int i1 = i + 1 < MT_N ? i + 1 : 0;
+    a = b;
+    if ((i & 1) == 0) {
+      hv = v;
+      const int w2 = i + 2 < MT_N ? i + 2 : i + 2 - MT_N;
+      const uint2 pa = pair(w2);
+      b = pa.x;
+      ha = pa.y;
+      const int k = i1 + MT_M < MT_N ? i1 + MT_M : i1 + MT_M - MT_N;  // even: pair (i+398, i+399)
+      const uint2 pb = pair(k);
+      j = pb.x;
+      hb = pb.y;
+    } else {
+      *reinterpret_cast<uint2*>(st + i - 1) = make_uint2(hv, v);
+      b = ha;
+      j = hb;
+    }
+    mti = i1;
+    v ^= (v >> 11);
+    v ^= (v << 7) & 0x9d2c5680u;
+    v ^= (v << 15) & 0xefc60000u;
+    v ^= (v >> 18);
+    return v;
+  }
+  __device__ __forceinline__ void finish() {
+    if (mti & 1) st[mti - 1] = hv;  // the last draw was even: its word is still held
+  }
+};
+__device__ __forceinline__ uint32_t mt_randbelow(ChainMt2& m, uint32_t n) {
+  const int k = 32 - __clz(n);
+  uint32_t r = m.next() >> (32 - k);
+  while (r >= n) r = m.next() >> (32 - k);
+  return r;
+}
+__device__ __forceinline__ double mt_random(ChainMt2& m) {
+  const uint32_t a = m.next() >> 5, b = m.next() >> 6;
+  return (a * 67108864.0 + b) * (1.0 / 9007199254740992.0);
+}
 __device__ __forceinline__ uint32_t mt_randbelow(ChainMt& m, uint32_t n) {
   const int k = 32 - __clz(n);
   uint32_t r = m.next() >> (32 - k);
@@ -1144,7 +1207,11 @@ __global__ void __launch_bounds__(128, SLOTS ? SIP_MINB_SLOTS : SIP_MINB) anneal
   if (c >= s.C) return;
   const typename RowOf<SLOTS>::T row = RowOf<SLOTS>::make(s, c, smem_raw);
   row.start(s);
+#ifdef SIP_MT_SCALAR
   ChainMt mt;  // chain-major row: a chain's draws stay in its own sectors
+#else
+  ChainMt2 mt;  // chain-major row read and written in pairs
+#endif
   mt.st = s.mt + (size_t)c * MT_N;
   {
     uint32_t key[2];
@@ -1226,6 +1293,9 @@ __global__ void __launch_bounds__(128, SLOTS ? SIP_MINB_SLOTS : SIP_MINB) anneal
   s.e_best[c] = e_best;
   s.best_iter[c] = best_iter;
   s.ambiguous[c] = amb;
+#ifndef SIP_MT_SCALAR
+  mt.finish();
+#endif
   s.mti[c] = mt.mti == 0 ? MT_N : mt.mti;  // 624: the next draw starts a round (rng.cuh)
   s.replayed[c] = steps;
   s.priced[c] = priced;
