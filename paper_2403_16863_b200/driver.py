@@ -19,8 +19,6 @@ from __future__ import annotations
 
 from dataclasses import dataclass, replace
 
-import numpy as np
-
 from .anneal import AnnealConfig, AnnealState, anneal_batch_sim, anneal_steps, uses_device_energy
 from .ir import Kernel
 from .perturb import candidates
@@ -122,8 +120,8 @@ def run_states(kernel: Kernel, backend, cfg: AnnealConfig, chains: int, tester=N
     if tables is None and hasattr(backend, "tables_for"):
         tables = backend.tables_for(kernel, cfg.candidate_classes)
     if tester is None and uses_device_energy(backend):
-        # consecutive seeds (driver.py:73-79) as one int64 array: no per-chain Python objects
-        seeds = np.arange(chains, dtype=np.int64) + np.int64(cfg.seed)
+        # consecutive seeds (driver.py:73-79) as a range: no per-chain host objects or arrays
+        seeds = range(cfg.seed, cfg.seed + chains)
         return anneal_batch_sim(kernel, backend.machine, cfg, seeds, tables=tables)
     seeds = [cfg.seed + c for c in range(chains)]
     if getattr(backend, "batched_chains", False):

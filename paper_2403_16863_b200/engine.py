@@ -435,18 +435,24 @@ class DeviceKernel:
         """Fused chains left entirely in HBM (sip_anneal_keep_reduced): only the device-reduced
         champion and sums come back; consecutive seeds are generated on the device.
         Returns (EpochResult dict, DeviceResults)."""
-        seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.int64))
+        if isinstance(seeds, range) and seeds.step == 1:
+            # run_search's consecutive seeds (driver.py:73-79) as a range: nothing per chain
+            # on the host (an int64 array of 227 k seeds and its np.diff check cost ~0.5 ms
+            # a step); the device generates them
+            C, consecutive, base = len(seeds), True, seeds.start
+        else:
+            seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.int64))
+            C = len(seeds)
+            consecutive = C > 0 and (C == 1 or bool(np.all(np.diff(seeds) == 1)))
+            base = int(seeds[0]) if consecutive else 0
         temps = np.ascontiguousarray(temps, dtype=np.float64)
-        C = len(seeds)
-        consecutive = C > 0 and (C == 1 or bool(np.all(np.diff(seeds) == 1)))
         st = None if start is None else np.ascontiguousarray(start, dtype=np.uint16)
         cfg = self._cfg(temps, unsafe, hw_safe, min_fixed)
         res = EpochResult()
         h = ctypes.c_void_p()
         self.ctx.check(self.ctx.lib.sip_anneal_keep_reduced(
             self.handle, ctypes.byref(cfg), None if consecutive else _ptr(seeds, c_i64p),
-            int(seeds[0]) if consecutive else 0, C, None if st is None else _ptr(st, c_u16p),
-            ctypes.byref(res), ctypes.byref(h)))
+            base, C, None if st is None else _ptr(st, c_u16p), ctypes.byref(res), ctypes.byref(h)))
         out = {f: getattr(res, f) for f, _ in EpochResult._fields_ if f != "pad"}
         return out, DeviceResults(self, h, C, len(temps))
 
