@@ -713,11 +713,11 @@ def main() -> None:
     dk = ctx.kernel(tables)
     acfg = AnnealConfig()  # reference defaults: T 1.0 -> 0.01, cooling 1.05, 95 iterations
     temps = acfg.temperatures()
-    # 12 blocks of 128 chains per SM (two waves at the dense kernel's 6 resident blocks, 1.7 at
-    # SlotRow's 7): measured best for the public-API (e2e) rate, chains from the nvcc schedule
-    # -- 2 full SlotRow waves (265 216 chains) gave 3.82e9 engine but 2.84e9 e2e, 227 328 gave
-    # 3.72e9 / 3.24e9, 132 608 3.50e9 / 3.05e9
-    C = args.sim_chains or 12 * 128 * ctx.sm_count
+    # 56 blocks of 128 chains per SM = 8 full waves of SlotRow chains (7 resident blocks): the
+    # last wave's tail (chains differ in length) shrinks with more waves.  Same box, engine /
+    # e2e x 1e9: 227 328 chains 3.88 / 3.81, 265 216 3.97 / 3.92, 397 824 4.10 / 4.07,
+    # 530 432 4.19 / 4.18, 795 648 4.30 / 4.29, 1 061 376 4.36 / 4.36
+    C = args.sim_chains or 56 * 128 * ctx.sm_count
     best = {"e": 1.0, "perm": None}
 
     def epoch(ep: int):
