@@ -826,9 +826,11 @@ def main() -> None:
                                    "the same kernel on the B200",
                        "chains_per_gpu": C, "step": "one epoch = 95 iterations of every chain + "
                                                     "NCCL allgather of (energy, seed) + champion broadcast",
-                       "l2": "engine chain state (~10 KB per chain, ~3 GB per GPU) is larger than "
-                             "L2, so every step streams it from HBM; the hardware phase flushes L2 "
-                             "(256 MB) before every timed launch",
+                       "l2": f"engine chain state ({dk.state_bytes(len(temps)) / 1e3:.1f} KB per chain, "
+                             f"{dk.state_bytes(len(temps)) * C / 1e9:.1f} GB per GPU) is far larger than "
+                             "L2, so every step streams it from HBM; the hardware phase rotates its "
+                             "launches over input sets whose combined size exceeds L2 (or flushes a "
+                             "256 MB buffer where that would take more than 64 sets)",
                        "parallelism": f"{world} GPU(s), independent chains, allgather per epoch"},
             "roofline": roofline, "engine": engine,
             "hw": gemm["hw"], "tuned": gemm["tuned"], "verify": gemm["verify"],
