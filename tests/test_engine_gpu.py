@@ -261,3 +261,28 @@ def test_no_candidates_raises_like_the_reference():
                      "[B------:R-:W-:-:S04] IADD3 R8, R9, 0x1, RZ ;\n", name="alu_only")
     with pytest.raises(NoCandidatesError):
         run_search(k, SimulatorBackend(), AnnealConfig(seed=0), chains=4)
+
+
+@pytest.mark.parametrize("name", ["gemm_lrelu_f16", "random_program_3", "corridor", "base_detect"])
+def test_slot_chains_equal_dense_rows(name, monkeypatch):
+    """SlotRow chains (candidate slots in shared memory, rows built on read) and dense-row
+    chains (SIP_NO_SLOTS=1) are the same search: histories, best and current schedules and
+    summaries are identical for the same seeds, on the decoded GEMM target listing (k = 5)
+    and on golden listings with 4-8 candidates."""
+    from pathlib import Path
+
+    if name == "gemm_lrelu_f16":
+        text = (Path(__file__).parent / "golden" / "listings" / f"{name}.sass").read_text()
+    else:
+        text = golden()["listings"][name]["text"]
+    k = parse_kernel(text, name=name)
+    t = KernelTables.build(k, MachineConfig())
+    assert 0 < len(t.global_ids) <= 8  # a SlotRow listing
+    dk = get_context().kernel(t)
+    temps = AnnealConfig().temperatures()
+    seeds = np.arange(5_000, 5_000 + 2_048, dtype=np.int64)
+    slots = dk.anneal(seeds, temps)
+    monkeypatch.setenv("SIP_NO_SLOTS", "1")
+    dense = dk.anneal(seeds, temps)
+    for a, b in zip(slots, dense):
+        assert np.array_equal(a, b)
