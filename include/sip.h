@@ -174,9 +174,10 @@ int sip_results_fetch(sip_results* r, int32_t first, int32_t count, sip_record* 
                       uint16_t* best, uint16_t* current);
 int sip_results_destroy(sip_results* r);
 
-/* device bytes one fused chain of `budget` iterations keeps in HBM (its working set:
- * schedules, MT19937 words, checkpoints, logs, history) -- the denominator of the
- * engine's DRAM-traffic ratio in bench.py */
+/* device bytes one fused chain of `budget` iterations works on in HBM during a launch
+ * (schedules -- or, for listings with at most 8 candidates, its candidate slots, the rows
+ * being built only when read --, MT19937 words, checkpoints, logs, history): the
+ * denominator of the engine's DRAM-traffic ratio in bench.py */
 int sip_anneal_state_bytes(sip_kernel* k, int32_t budget, int64_t* per_chain);
 
 /* chains that fill every SM once with the fused simulator-energy kernel (one
