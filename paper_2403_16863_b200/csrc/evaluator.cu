@@ -663,6 +663,11 @@ int sip_measure_round(sip_module* m, const uint16_t* perm_ref, const uint16_t* p
                        : measure_round_streamed(m, perm_ref, perms, k, L, nL, warmup, reps, flush_l2,
                                                 ratio_median, ref_median_ms, cand_median_ms, raw_ratio, status);
   for (auto& c : m->cache) c.pinned = false;
+  while (m->cache.size() > m->cache_cap) {  // the round is done: unloading no longer stalls it
+    const size_t before = m->cache.size();
+    evict_one(m);
+    if (m->cache.size() == before) break;
+  }
   return rc;
 }
 
@@ -1004,7 +1009,9 @@ static int measure_round_streamed(sip_module* m, const uint16_t* perm_ref, const
       cm.fn = fns[t];
       cm.stamp = ++m->clock;
       cm.pinned = true;
-      if (m->cache.size() >= m->cache_cap) evict_one(m);
+      // no eviction while the device runs this round's launches: cuModuleUnload waits for
+      // the context's pending work, which would stall the pipeline once per candidate; the
+      // cache is trimmed after the round (sip_measure_round)
       mods[i] = insert_module(m, std::move(cm));
       ++t;
     }
