@@ -663,7 +663,11 @@ int sip_measure_round(sip_module* m, const uint16_t* perm_ref, const uint16_t* p
                        : measure_round_streamed(m, perm_ref, perms, k, L, nL, warmup, reps, flush_l2,
                                                 ratio_median, ref_median_ms, cand_median_ms, raw_ratio, status);
   for (auto& c : m->cache) c.pinned = false;
-  while (m->cache.size() > m->cache_cap) {  // the round is done: unloading no longer stalls it
+  // the round is done, so unloading no longer stalls it: keep the most recent modules only
+  // (a driver holding thousands of modules loads new ones more slowly; SIP_MODULE_KEEP)
+  static const size_t keep = getenv("SIP_MODULE_KEEP") ? (size_t)atol(getenv("SIP_MODULE_KEEP")) : 64;
+  m->cache_cap = std::max<size_t>(keep, 4);
+  while (m->cache.size() > m->cache_cap) {
     const size_t before = m->cache.size();
     evict_one(m);
     if (m->cache.size() == before) break;

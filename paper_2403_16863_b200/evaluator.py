@@ -12,6 +12,7 @@ or launch failure raises ``MeasurementFailed``.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 
@@ -23,6 +24,9 @@ from .targets import cold_sets, launch_sets, make_target
 
 FIXED_LAT_HEAVY = ("HMMA", "IMMA", "DMMA", "BMMA", "HGMMA", "DFMA", "DADD", "DMUL")
 
+
+# candidates per sip_measure_round call (big search rounds are split; SIP_ROUND_CHUNK)
+ROUND_CHUNK = int(os.environ.get("SIP_ROUND_CHUNK", "64"))
 
 def min_fixed_distance(kernel: Kernel) -> int:
     """Issue distance (cycles) a fixed-latency producer must keep to its consumer
@@ -122,6 +126,14 @@ class B200Backend:
         k = perms.shape[0]
         if k == 0:
             return []
+        if self.rounds and k > ROUND_CHUNK:
+            # a driver holding thousands of modules loads new ones several times slower: big
+            # rounds are timed in chunks, each with its own nvcc reference in the rotation and
+            # its modules unloaded before the next
+            out = []
+            for i in range(0, k, ROUND_CHUNK):
+                out.extend(self.measure_batch(perms[i:i + ROUND_CHUNK], reps))
+            return out
         if not self.paired:
             return [self._try(lambda p=p: self._measure_single(p, reps)) for p in perms]
         ratio, refm, candm = (np.zeros(k, dtype=np.float64) for _ in range(3))

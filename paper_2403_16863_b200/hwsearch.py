@@ -73,7 +73,9 @@ class HardwareSearch:
             n += 1
             self.launches += (1 if getattr(self.be, "rounds", False) else 2) * (self.be.warmup + self.cfg.measure_reps)
         if n and getattr(self.be, "rounds", False):
-            self.launches += self.be.warmup + self.cfg.measure_reps  # the round's one nvcc reference
+            from .evaluator import ROUND_CHUNK
+            chunks = -(-len(live) // ROUND_CHUNK)  # one nvcc reference per measured chunk
+            self.launches += chunks * (self.be.warmup + self.cfg.measure_reps)
         if len(live):
             self.chains.resolve(self.times, self.status)
             self.launches += 1
