@@ -306,6 +306,23 @@ def test_measure_round_and_legacy_batch(shape, rounds):
         assert len(smp.raw) == 5 and 0.9 * be.ref_ms < smp.value < 1.1 * be.ref_ms
 
 
+def test_measure_round_in_chunks():
+    """A round larger than ROUND_CHUNK is timed in chunks, each with its own nvcc reference:
+    every candidate is priced (identical schedules at ratio ~1) and the module cache is
+    trimmed back afterwards."""
+    from paper_2403_16863_b200.evaluator import ROUND_CHUNK
+
+    tgt = GemmTarget(M=512, N=512, K=512).allocate()
+    be = B200Backend(tgt, rounds=True)
+    ident = schedule_perm(be.kernel)
+    k = ROUND_CHUNK + 7
+    out = be.measure_batch(np.stack([ident] * k), reps=3)
+    assert len(out) == k
+    for smp in out:
+        assert not isinstance(smp, Exception)
+        assert 0.8 * be.ref_ms < smp.value < 1.25 * be.ref_ms
+
+
 def test_measure_batch_module_cache_churn():
     """Batches larger than the module cache, repeated, with the baseline schedule itself
     among the candidates: no module a batch still launches may be evicted (a dangling
