@@ -1776,7 +1776,10 @@ int sip_kernel_create(sip_ctx* ctx, const sip_tables* t, sip_kernel** out) {
   d.k = (int)gids.size();
   std::vector<uint8_t> pin(n, 0);
   if (t->pin) std::memcpy(pin.data(), t->pin, n);
-  std::vector<int32_t> cum(n, 0);  // issue prefix sums of the listing (nvcc) order
+  // issue prefix sums of the listing order, which hw_safe takes as ptxas-proven distances:
+  // the nvcc schedule, or a schedule reached from it under hw_safe (every pair it moved kept
+  // at least min(limit, its nvcc distance), so the bound carries over by induction)
+  std::vector<int32_t> cum(n, 0);
   for (size_t i = 1; i < n; ++i) cum[i] = cum[i - 1] + (int32_t)c_adv(t->ctrl[i - 1]);
   int rc = SIP_OK;
   if ((rc = dalloc(ctx, &d.meta, n)) || (rc = dalloc(ctx, &d.klass, n)) ||
