@@ -57,7 +57,8 @@ def parse():
     ap.add_argument("--sim-chains", type=int, default=0,
                     help="engine chains per GPU (0: two full waves of the fused kernel, "
                          "sip_anneal_wave; 303 104 on a 148-SM B200)")
-    ap.add_argument("--chains", type=int, default=16, help="hardware-priced chains per GPU")
+    ap.add_argument("--chains", type=int, default=128,
+                    help="hardware-priced chains per GPU (more candidates per round amortise its nvcc reference)")
     ap.add_argument("--hw-steps", type=int, default=24, help="hardware search rounds")
     ap.add_argument("--classes", default="extended", choices=["global", "extended", "sm100"],
                     help="hardware-phase candidate classes: the reference's (global) or the "
