@@ -5,7 +5,7 @@ TAG=${1:-fin}
 bash tools/gpu_full.sh $TAG
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${TAG}_ref.log 2>&1
 echo "ref rc=$?" >> gpurun_out/${TAG}_ref.log
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 30000 --csv \
   --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 3 --hw-steps 4 --attn-steps 2 --verify-samples 100000 --cpu-seconds 1 --no-e2e > gpurun_out/${TAG}_ncu_bench.log 2>&1
 echo "ncu rc=$?" >> gpurun_out/${TAG}_ncu_bench.log
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:anneal_fused -s 1 -c 1 \
