@@ -251,7 +251,10 @@ int sip_measure_paired(sip_module* m, const uint16_t* perm_ref, const uint16_t* 
  * reference and the k candidates are warmed up once each, then each of `reps` reps launches
  * all k+1 modules once in a rotated order, event-timed; candidate i's ratio is the median
  * over reps of t_i / t_ref of the same rep.  Launch slot q uses parameter set L[q % nL]
- * (nL >= 3 buffer sets larger than L2 in rotation need no flush: flush_l2 = 0).
+ * (nL >= 3 buffer sets larger than L2 in rotation need no flush: flush_l2 = 0).  The
+ * candidates' modules load on worker threads while the warm-ups already run, and the
+ * launches go straight onto the stream (SIP_ROUND_GRAPH=1: one captured CUDA graph after
+ * all loads); afterwards the module cache keeps the 64 most recent (SIP_MODULE_KEEP).
  * Replaces backends.ExternalCommandBackend.measure per candidate (backends.py:66-116). */
 int sip_measure_round(sip_module* m, const uint16_t* perm_ref, const uint16_t* perms, int32_t k,
                       const sip_launch* L, int32_t nL, int32_t warmup, int32_t reps, int32_t flush_l2,
