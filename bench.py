@@ -589,8 +589,9 @@ def hardware_phase(kind, listing, local, rank, world, dist, args, rounds, shape=
           "t_kernel_ms": avg_ms, "warm_launch_ms": warm_ms,
           "cold_input_sets": be.nsets,
           "note": ("one round = the live chains' candidates re-encoded and loaded with cuModuleLoadData "
-                   "(8 host threads), then ONE CUDA graph: every candidate and one nvcc reference warmed "
-                   "up (2 launches each) and launched 5 times in rotated order with an event pair each; "
+                   "on 8 host threads while the device already runs the warm-ups of the modules loaded so "
+                   "far (streamed round, chunks of <= 64 candidates): every candidate and one nvcc reference "
+                   "warmed up (2 launches each), then launched 5 times in rotated order with an event pair each; "
                    "energy = median over reps of t_cand / t_ref in the same rep. Launches rotate over "
                    f"{be.nsets} input sets so no launch finds its inputs in L2 (no flush). Roofline = "
                    "1 / ((warmup + reps) * T_kernel), T_kernel = average timed launch")}

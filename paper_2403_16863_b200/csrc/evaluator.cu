@@ -258,22 +258,33 @@ bool strip_debug(const std::vector<uint8_t>& img, const std::vector<Sec>& secs, 
   return ok;
 }
 
-int build_image(sip_module* m, const uint16_t* perm, std::vector<uint8_t>& out, bool for_load = true) {
-  out = for_load ? m->load_image : m->image;
-  const uint64_t toff = for_load ? m->load_text_off : m->text_off;
-  if (perm) {
-    const uint8_t* src = m->image.data() + m->text_off;
-    uint8_t* dst = out.data() + toff;
-    std::vector<uint8_t> seen(m->n, 0);
-    for (int i = 0; i < m->n; ++i) {
-      int p = perm[i];
-      if (p < 0 || p >= m->n || seen[p]) return sip::fail(m->ctx, SIP_E_ARG, "perm is not a permutation");
-      seen[p] = 1;
-      std::memcpy(dst + 16 * (size_t)i, src + 16 * (size_t)p, 16);
-    }
+bool is_permutation(const sip_module* m, const uint16_t* perm) {
+  std::vector<uint8_t> seen(m->n, 0);
+  for (int i = 0; i < m->n; ++i) {
+    const int p = perm[i];
+    if (p >= m->n || seen[p]) return false;
+    seen[p] = 1;
   }
-  // images the driver loads drop the merc sections; a patched cubin written out keeps them
-  return for_load ? neutralize_merc(m, out) : SIP_OK;
+  return true;
+}
+
+// the image for schedule `perm` (a permutation the caller has checked): the template's
+// .text words gathered in schedule order.  Touches no shared state, so the evaluator's
+// worker threads build their candidates' images themselves.
+void gather_image(const sip_module* m, const uint16_t* perm, std::vector<uint8_t>& out, bool for_load) {
+  out = for_load ? m->load_image : m->image;
+  if (!perm) return;
+  const uint8_t* src = m->image.data() + m->text_off;
+  uint8_t* dst = out.data() + (for_load ? m->load_text_off : m->text_off);
+  for (int i = 0; i < m->n; ++i) std::memcpy(dst + 16 * (size_t)i, src + 16 * (size_t)perm[i], 16);
+}
+
+int build_image(sip_module* m, const uint16_t* perm, std::vector<uint8_t>& out, bool for_load = true) {
+  if (perm && !is_permutation(m, perm)) return sip::fail(m->ctx, SIP_E_ARG, "perm is not a permutation");
+  // the load image already had its merc sections renamed at sip_module_open; a patched
+  // cubin written out keeps them
+  gather_image(m, perm, out, for_load);
+  return SIP_OK;
 }
 
 int cu_fail(sip_ctx* ctx, int code, const char* what, CUresult r) {
@@ -472,6 +483,11 @@ int sip_module_open(sip_ctx* ctx, const void* cubin, size_t size, const char* fu
       m->load_image.swap(stripped);
       m->load_text_off = s2[tidx].off;
     }
+  }
+  // images the driver loads drop the merc sections (renamed once here, not per candidate)
+  if (int rc = neutralize_merc(m, m->load_image); rc != SIP_OK) {
+    delete m;
+    return rc;
   }
   *out = m;
   return SIP_OK;
@@ -720,7 +736,7 @@ static int load_batch(sip_module* m, const uint16_t* perm_ref, const uint16_t* p
   std::vector<CUmodule> loaded(todo.size(), nullptr);
   std::vector<CUresult> lres(todo.size(), CUDA_SUCCESS);
   for (size_t t = 0; t < todo.size(); ++t)
-    if (build_image(m, perms + (size_t)todo[t] * m->n, imgs[t]) != SIP_OK) lres[t] = CUDA_ERROR_INVALID_IMAGE;
+    if (!is_permutation(m, perms + (size_t)todo[t] * m->n)) lres[t] = CUDA_ERROR_INVALID_IMAGE;
   // the loads run in this thread's CUDA context (made current in each worker), so the
   // modules belong to the context the launches below use
   CUcontext cur = nullptr;
@@ -736,8 +752,10 @@ static int load_batch(sip_module* m, const uint16_t* perm_ref, const uint16_t* p
     pool.emplace_back([&, w]() {
       const bool ctx_ok = ctx->cuCtxSetCurrent(cur) == CUDA_SUCCESS;
       for (size_t t = w; t < todo.size(); t += nthreads)
-        if (lres[t] == CUDA_SUCCESS)
+        if (lres[t] == CUDA_SUCCESS) {  // each worker gathers its own images (gather_image)
+          gather_image(m, perms + (size_t)todo[t] * m->n, imgs[t], /*for_load=*/true);
           lres[t] = ctx_ok ? ctx->cuModuleLoadData(&loaded[t], imgs[t].data()) : CUDA_ERROR_INVALID_CONTEXT;
+        }
     });
   for (auto& th : pool) th.join();
   for (size_t t = 0; t < todo.size(); ++t) {
@@ -962,10 +980,10 @@ static int measure_round_streamed(sip_module* m, const uint16_t* perm_ref, const
   std::vector<CUmodule> loaded(nt, nullptr);
   std::vector<CUfunction> fns(nt, nullptr);
   std::unique_ptr<std::atomic<int>[]> ready(new std::atomic<int>[nt > 0 ? nt : 1]);
-  for (size_t t = 0; t < nt; ++t) {
-    ready[t].store(0);
-    if (build_image(m, perms + (size_t)todo[t] * m->n, imgs[t]) != SIP_OK) ready[t].store(-1);
-  }
+  // only the check runs here; each worker gathers its candidates' images itself, so the
+  // first module reaches the device after one image and one load, not after all k images
+  for (size_t t = 0; t < nt; ++t)
+    ready[t].store(is_permutation(m, perms + (size_t)todo[t] * m->n) ? 0 : -1);
   CUcontext cur = nullptr;
   if (ctx->cuCtxGetCurrent(&cur) != CUDA_SUCCESS || cur == nullptr) {
     SIP_CUDA(ctx, cudaFree(nullptr));
@@ -979,8 +997,10 @@ static int measure_round_streamed(sip_module* m, const uint16_t* perm_ref, const
     pool.emplace_back([&, w]() {
       const bool ctx_ok = ctx->cuCtxSetCurrent(cur) == CUDA_SUCCESS;
       for (size_t t = w; t < nt; t += nthreads) {
-        if (ready[t].load() != 0) continue;  // image could not be built
+        if (ready[t].load() != 0) continue;  // not a permutation
+        gather_image(m, perms + (size_t)todo[t] * m->n, imgs[t], /*for_load=*/true);
         bool ok = ctx_ok && ctx->cuModuleLoadData(&loaded[t], imgs[t].data()) == CUDA_SUCCESS;
+        std::vector<uint8_t>().swap(imgs[t]);  // the driver keeps its own copy
         if (ok && ctx->cuModuleGetFunction(&fns[t], loaded[t], m->func.c_str()) != CUDA_SUCCESS) {
           ctx->cuModuleUnload(loaded[t]);
           loaded[t] = nullptr;
