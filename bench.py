@@ -59,6 +59,10 @@ def parse():
                          "sip_anneal_wave; 303 104 on a 148-SM B200)")
     ap.add_argument("--chains", type=int, default=128,
                     help="hardware-priced chains per GPU (more candidates per round amortise its nvcc reference)")
+    ap.add_argument("--refill", type=int, default=0,
+                    help="hardware phase: start a cohort of this many fresh chains whenever that many "
+                         "chain slots are idle (finished chains), so every round prices a full set "
+                         "of candidates (0: one cohort, run until its chains finish)")
     ap.add_argument("--hw-steps", type=int, default=24, help="hardware search rounds")
     ap.add_argument("--classes", default="extended", choices=["global", "extended", "sm100"],
                     help="hardware-phase candidate classes: the reference's (global) or the "
@@ -475,10 +479,13 @@ def warm_launch_ms(be, n: int, reps: int = 10) -> float:
     return med.value
 
 
-def library_tflops(kind, tgt, reps: int = 15) -> dict:
+def library_tflops(kind, tgt, be, n: int, rounds: int = 6, reps: int = 5) -> dict:
     """Context only: the same operation through the vendor library on the same inputs
-    (torch.matmul -> cuBLAS; scaled_dot_product_attention -> cuDNN/flash), median of
-    `reps` launches with the same 256 MB L2 flush before each."""
+    (torch.matmul -> cuBLAS; scaled_dot_product_attention -> cuDNN/flash), timed like for
+    like with the nvcc schedule of our kernel: `rounds` alternating rounds of `reps` launches
+    each, a 256 MB L2 flush before every launch on both sides, so both see the same power
+    state and clocks; medians over all launches."""
+    import numpy as np
     import torch
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=tgt.inputs[0].device)
@@ -494,17 +501,23 @@ def library_tflops(kind, tgt, reps: int = 15) -> dict:
         name = "torch scaled_dot_product_attention, fp16, non-causal"
     for _ in range(3):
         fn()
-    ts = []
-    for _ in range(reps):
-        flush.fill_(1)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        fn()
-        e1.record()
-        e1.synchronize()
-        ts.append(e0.elapsed_time(e1))
-    ms = statistics.median(ts)
-    return {"tflops": tgt.flops / ms / 1e9, "ms": ms, "what": name}
+    ident = np.arange(n, dtype=np.uint16)
+    lib_ms, ours_ms = [], []
+    for _ in range(rounds):
+        for _ in range(reps):
+            flush.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            lib_ms.append(e0.elapsed_time(e1))
+        ours_ms.extend(be._measure_single(ident, reps).raw)
+    ms, ours = statistics.median(lib_ms), statistics.median(ours_ms)
+    return {"tflops": tgt.flops / ms / 1e9, "ms": ms, "what": name,
+            "ours_nvcc_ms": ours, "ours_nvcc_tflops": tgt.flops / ours / 1e9, "library_over_ours": ours / ms,
+            "method": f"{rounds} alternating rounds of {reps} flushed launches each (library, then the nvcc "
+                      "schedule of our kernel through sip_measure); medians"}
 
 
 FULL_SHAPE_INPUTS = 16  # independent Philox input sets compared at the tuned shape
@@ -532,7 +545,7 @@ def hardware_phase(kind, listing, local, rank, world, dist, args, rounds, shape=
     # clocks are sampled over the whole phase (nvidia-smi needs ~0.5 s to deliver its
     # first sample; the timed rounds alone can be shorter than that)
     hclk = ClockSampler(local).__enter__()
-    hs = HardwareSearch(be, hcfg, args.chains, epoch=args.epoch, dist=dist)
+    hs = HardwareSearch(be, hcfg, args.chains, epoch=args.epoch, dist=dist, refill=args.refill)
     hs.step()
     be.kernel_ms.clear()
     launches0, evald0 = hs.launches, hs.evaluated
@@ -582,8 +595,9 @@ def hardware_phase(kind, listing, local, rank, world, dist, args, rounds, shape=
     floor_ms = (be.warmup + hcfg.measure_reps) * avg_ms
     rate = h_eval / (h_ms / 1e3)
     hw = {"candidates_per_s": rate, "rounds": rounds, "chains_per_gpu": args.chains,
+          "refill": args.refill, "chains_started": len(hs.seeds),
           "candidate_classes": args.classes, "candidates_in_listing": int(hs.dk.k),
-          "proposals": rounds * args.chains * world, "priced": int(h_eval),
+          "chain_rounds": rounds * args.chains * world, "priced": int(h_eval),
           "evaluator_roofline_candidates_per_s": world * 1e3 / floor_ms,
           "device_busy_frac": rate / (world * 1e3 / floor_ms),
           "t_kernel_ms": avg_ms, "warm_launch_ms": warm_ms,
@@ -624,7 +638,7 @@ def hardware_phase(kind, listing, local, rank, world, dist, args, rounds, shape=
                  "rejected_by_verification": [{"energy": e, "first_failing_sample": v.first_fail_sample,
                                                "max_abs_err": v.max_abs_err} for e, v in rejected],
                  "paper_speedup": 1.1227 if kind == "gemm" else 1.062,
-                 "library_tflops": library_tflops(kind, tgt)}
+                 "library_tflops": library_tflops(kind, tgt, be, n)}
     # every rank verifies its share of the samples (batches rank, rank+world, ...) of the
     # same champion; (passed, failed) sum and the first failing sample is the min over ranks
     best = acc_perm

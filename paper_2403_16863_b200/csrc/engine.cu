@@ -1385,14 +1385,19 @@ __global__ void __launch_bounds__(128) chains_propose_kernel(KernelDev d, Chains
   s.p_cand[c] = (uint16_t)cand;
   s.p_dir[c] = (uint8_t)dir;
   lo_out[c] = lo;
-  if (s.cand_out != nullptr && lo >= 0) {
-    uint16_t* out = s.cand_out + (size_t)c * s.n;
-    const uint16_t* row = s.sched + (size_t)c * s.ns;
-    for (int p = 0; p < s.n; ++p) out[p] = row[p];
-    uint16_t t = out[lo];
-    out[lo] = out[lo + 1];
-    out[lo + 1] = t;
-  }
+}
+
+// the proposed candidate schedules (current row with the pair at lo swapped), one warp per
+// chain with lane-strided, coalesced accesses: a per-thread copy had each warp store touch
+// 32 rows and made the row copy most of a propose call
+__global__ void cand_rows_kernel(Chains s, const int32_t* lo_in) {
+  const int c = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (c >= s.C) return;
+  const int lo = lo_in[c];
+  if (lo < 0) return;
+  const uint16_t* row = s.sched + (size_t)c * s.ns;
+  uint16_t* out = s.cand_out + (size_t)c * s.n;
+  for (int p = lane; p < s.n; p += 32) out[p] = row[p == lo ? lo + 1 : p == lo + 1 ? lo : p];
 }
 
 __global__ void chains_resolve_kernel(KernelDev d, Chains s, const double* t_curr,
@@ -2224,6 +2229,10 @@ int sip_chains_propose(sip_chains* o, int32_t* lo, uint16_t* sched) {
   chains_propose_kernel<<<(C + 127) / 128, 128, use_smem ? sm : 0, ctx->stream>>>(k->d, o->s,
                                                                                  use_smem, o->d_lo);
   SIP_CHECK_LAUNCH(ctx);
+  if (sched && o->s.cand_out) {
+    cand_rows_kernel<<<(C + 3) / 4, 128, 0, ctx->stream>>>(o->s, o->d_lo);
+    SIP_CHECK_LAUNCH(ctx);
+  }
   TRY(d2h(ctx, lo, o->d_lo, C));
   if (sched) TRY(d2h(ctx, sched, o->s.cand_out, (size_t)C * k->d.n));
   SIP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
