@@ -35,6 +35,7 @@ class _Cohort:
         self.times = np.zeros(self.C, dtype=np.float64)
         self.status = np.zeros(self.C, dtype=np.uint8)
         self.done = False  # every chain has spent its iteration budget
+        self.final = None  # (hist, best, cur, summ) of a finished cohort, fetched once
 
 
 class HardwareSearch:
@@ -165,9 +166,20 @@ class HardwareSearch:
         except MeasurementFailed as exc:
             return exc
 
+    def _result_of(self, co):
+        if co.final is not None:
+            return co.final
+        res = co.sc.result()
+        if co.done and self.refill:
+            # a finished cohort never changes again (exchange adopts into live cohorts
+            # only): keep its results on the host and release its device chains, so a long
+            # refilled search holds device state for its live chains only
+            co.final, co.sc = res, None
+        return res
+
     def _results(self):
         """(hist, best, cur, summ) over every chain of every cohort, in seed-list order."""
-        parts = [co.sc.result() for co in self.cohorts]
+        parts = [self._result_of(co) for co in self.cohorts]
         if len(parts) == 1:
             return parts[0]
         return tuple(np.concatenate([p[i] for p in parts]) for i in range(4))

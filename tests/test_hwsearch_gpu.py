@@ -69,7 +69,8 @@ def test_refill_cohorts_equal_standalone_chains(backend):
         alone = HardwareSearch(sp, CFG, len(co.seeds), seed0=co.seeds[0])
         assert alone.seeds == co.seeds
         _run_to_end(alone)
-        h1, b1, _, s1 = co.sc.result()
+        h1, b1, _, s1 = hs._result_of(co)  # a finished cohort: fetched once, device chains released
+        assert co.sc is None and co.final is not None
         h2, b2, _, s2 = alone.chains.result()
         assert np.array_equal(h1, h2)
         assert np.array_equal(b1, b2)
