@@ -55,8 +55,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--sim-chains", type=int, default=0,
-                    help="engine chains per GPU (0: two full waves of the fused kernel, "
-                         "sip_anneal_wave; 303 104 on a 148-SM B200)")
+                    help="engine chains per GPU (0: 16 full waves of SlotRow chains, 112 blocks of "
+                         "128 per SM; 2 121 728 on a 148-SM B200)")
     ap.add_argument("--chains", type=int, default=128,
                     help="hardware-priced chains per GPU (more candidates per round amortise its nvcc reference)")
     ap.add_argument("--refill", type=int, default=0,
@@ -729,11 +729,12 @@ def main() -> None:
     dk = ctx.kernel(tables)
     acfg = AnnealConfig()  # reference defaults: T 1.0 -> 0.01, cooling 1.05, 95 iterations
     temps = acfg.temperatures()
-    # 56 blocks of 128 chains per SM = 8 full waves of SlotRow chains (7 resident blocks): the
-    # last wave's tail (chains differ in length) shrinks with more waves.  Same box, engine /
-    # e2e x 1e9: 227 328 chains 3.88 / 3.81, 265 216 3.97 / 3.92, 397 824 4.10 / 4.07,
-    # 530 432 4.19 / 4.18, 795 648 4.30 / 4.29, 1 061 376 4.36 / 4.36
-    C = args.sim_chains or 56 * 128 * ctx.sm_count
+    # 112 blocks of 128 chains per SM = 16 full waves of SlotRow chains (7 resident blocks):
+    # the last wave's tail (chains differ in length) shrinks with more waves.  Same box,
+    # engine / e2e x 1e9: 227 328 chains 3.88 / 3.81, 265 216 3.97 / 3.92, 397 824 4.10 /
+    # 4.07, 530 432 4.19 / 4.18, 795 648 4.30 / 4.29, 1 060 864 4.38 / 4.38, 1 591 296
+    # 4.46 / 4.47, 2 121 728 4.50 / 4.51
+    C = args.sim_chains or 112 * 128 * ctx.sm_count
     best = {"e": 1.0, "perm": None}
 
     def epoch(ep: int):

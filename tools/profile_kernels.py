@@ -26,7 +26,7 @@ elif which == "engine":
     dk = get_context().kernel(KernelTables.build(L.kernel, MachineConfig()))
     temps = AnnealConfig().temperatures()
     C = int(sys.argv[2]) if len(sys.argv) > 2 else 0
-    C = C or 56 * 128 * get_context().sm_count  # the bench default (bench.py)
+    C = C or 112 * 128 * get_context().sm_count  # the bench default (bench.py)
     for r in range(2):  # the bench's epoch call (history recorded); ncu captures the second
         res, _ = dk.anneal_epoch_reduced(r * C, C, temps)
         print("launch", r, "chains", C, "priced", res["priced"], "replayed", res["replayed"], flush=True)
