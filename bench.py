@@ -201,7 +201,7 @@ def engine_roofline(cand_per_s: float, chains: int, state_bytes: int, sm_mhz) ->
 def engine_at_realistic_k(ctx, gemm_listing, temps, dist, world, steps: int = 3) -> dict:
     """The same engine and metric with the sm_100 extension classes, where the
     listings have hundreds of candidates instead of the reference classes' five: the GEMM
-    listing and the attention listing, eight full waves of chains each, histories recorded."""
+    listing and the attention listing, sixteen full waves of chains each, histories recorded."""
     import torch
 
     from paper_2403_16863_b200.cubin import render_listing
@@ -214,7 +214,7 @@ def engine_at_realistic_k(ctx, gemm_listing, temps, dist, world, steps: int = 3)
     attn = render_listing((TARGET_DIR / "attn_fwd.cubin").read_bytes(), "attn_fwd_f16")
     for name, lst in (("gemm_lrelu_f16", gemm_listing), ("attn_fwd_f16", attn)):
         dk = ctx.kernel(KernelTables.build(lst.kernel, MachineConfig(), classes="extended"))
-        C = 8 * dk.wave_chains()  # eight full waves, as the headline (chain-count sweep, DESIGN s4)
+        C = 16 * dk.wave_chains()  # sixteen full waves, as the headline (chain-count sweep, DESIGN s4)
         for w in range(2):
             dk.anneal_epoch_reduced(10_000_000 + w * C, C, temps)
         torch.cuda.synchronize()
