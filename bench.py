@@ -630,8 +630,12 @@ def hardware_phase(kind, listing, local, rank, world, dist, args, rounds, shape=
         t_nvcc = be._measure_single(ident, 15).value
         t_best = t_nvcc * ratio
         q1, q3 = np.percentile(raw, [25, 75])
+        # the spread of single pairs (IQR) vs the uncertainty of their median: a seeded
+        # bootstrap of the median over the 45 pair ratios
+        boot = np.median(np.random.default_rng(0).choice(np.asarray(raw), (2000, len(raw))), axis=1)
+        b_lo, b_hi = np.percentile(boot, [2.5, 97.5])
         tuned = {"nvcc_ms": t_nvcc, "best_ms": t_best, "speedup": 1.0 / ratio,
-                 "speedup_iqr": [1.0 / q3, 1.0 / q1], "pairs": 45,
+                 "speedup_iqr": [1.0 / q3, 1.0 / q1], "speedup_ci95": [1.0 / b_hi, 1.0 / b_lo], "pairs": 45,
                  "nvcc_tflops": tgt.flops / t_nvcc / 1e9, "best_tflops": tgt.flops / t_best / 1e9,
                  "instructions_moved": int((best != ident).sum()),
                  "search_best_energy": res["best_energy"], "accepted_energy": acc_e,
