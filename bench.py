@@ -626,7 +626,9 @@ def hardware_phase(kind, listing, local, rank, world, dist, args, rounds, shape=
     if rank == 0:
         ident = np.arange(n, dtype=np.uint16)
         best = acc_perm
-        ratio, raw = be.ratio(best, 45)  # paired: nvcc and best schedules alternate in one graph
+        # re-timed with the protocol that priced it: nvcc and best schedules alternate over 45
+        # reps, launches rotated over cold input sets (a 256 MB flush where a target needs it)
+        ratio, raw = be.ratio_round(best, 45)
         t_nvcc = be._measure_single(ident, 15).value
         t_best = t_nvcc * ratio
         q1, q3 = np.percentile(raw, [25, 75])

@@ -118,6 +118,29 @@ class B200Backend:
         self.kernel_ms.extend([ref_med.value] * reps + [cand_med.value] * reps)
         return r_med.value, raw.tolist()
 
+    def ratio_round(self, perm, reps: int = 45) -> tuple:
+        """Median cand/ref time ratio over `reps` reps of a one-candidate measurement round
+        (sip_measure_round): the same protocol that priced the candidate in the search --
+        the two schedules alternate (order rotated every rep), launches rotate over cold
+        input sets instead of a flush.  Returns (median ratio, per-rep ratios)."""
+        if not (self.rounds and self.nsets):
+            return self.ratio(perm, reps)
+        perm = np.ascontiguousarray(np.asarray(perm, dtype=np.uint16).reshape(1, self.listing.n))
+        ratio, refm, candm = (np.zeros(1, dtype=np.float64) for _ in range(3))
+        raw = np.zeros((1, reps), dtype=np.float64)
+        status = np.zeros(1, dtype=np.int32)
+        lib = self.ctx.lib
+        rc = lib.sip_measure_round(
+            self.module.handle, self.identity.ctypes.data_as(c_u16p), perm.ctypes.data_as(c_u16p), 1,
+            self._set_array, len(self._sets), self.warmup, reps, 0,
+            ratio.ctypes.data_as(c_dblp), refm.ctypes.data_as(c_dblp), candm.ctypes.data_as(c_dblp),
+            raw.ctypes.data_as(c_dblp), status.ctypes.data_as(c_i32p))
+        self.calls += 1
+        if rc == SIP_E_MEASURE or status[0] != 0:
+            raise MeasurementFailed(lib.sip_last_error(self.ctx.handle).decode(errors="replace"))
+        self.ctx.check(rc)
+        return float(ratio[0]), raw[0].tolist()
+
     def measure_batch(self, perms, reps: int = 5) -> list:
         """Paired timing of many candidates in one CUDA graph (sip_measure_paired_batch).
         Returns one CostSample per candidate, or a MeasurementFailed instance for a

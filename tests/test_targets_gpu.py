@@ -306,6 +306,18 @@ def test_measure_round_and_legacy_batch(shape, rounds):
         assert len(smp.raw) == 5 and 0.9 * be.ref_ms < smp.value < 1.1 * be.ref_ms
 
 
+def test_ratio_round_retimes_with_the_search_protocol():
+    """Re-timing through a one-candidate round (cold input sets, rotated order): the nvcc
+    schedule against itself is a ratio of ~1 with one ratio per rep."""
+    tgt = GemmTarget(M=2048, N=2048, K=2048).allocate()
+    be = B200Backend(tgt, rounds=True)
+    assert be.nsets >= 3
+    ident = schedule_perm(be.kernel)
+    r, raw = be.ratio_round(ident, 15)
+    assert len(raw) == 15 and 0.97 < r < 1.03
+    assert 0.97 < float(np.median(raw)) < 1.03
+
+
 def test_measure_round_in_chunks():
     """A round larger than ROUND_CHUNK is timed in chunks, each with its own nvcc reference:
     every candidate is priced (identical schedules at ratio ~1) and the module cache is
