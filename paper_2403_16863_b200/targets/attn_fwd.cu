@@ -307,21 +307,22 @@ attn_fwd_f16(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CU
           m_used = m_new;
         }
         // rescale O_X (rare) before any P of this step is published: PV_X(t-1) must be
-        // complete; the first half of PV_X(t) waits for p_full below
+        // complete; the first half of PV_X(t) waits for p_full below.  tcgen05.ld/st are
+        // warp-collective (.sync.aligned): every lane of a warp with a growing row runs the
+        // loop, the others with alpha = 1 (x * 1 == x).  Guarding it per lane deadlocked
+        // the kernel once rows grew often (inputs with sigma >= 2).
         const bool rescale = __any_sync(0xffffffffu, grow && t > 0);
         if (rescale) {
           mbar_wait(&o_done[x], (g - 1) & 1);
           tc_fence_after();
-          if (grow && t > 0) {
 #pragma unroll 1
-            for (int c = 0; c < HD / 32; ++c) {
-              uint32_t v[32];
-              tmem_ld32(tO(x) + lane_off + c * 32, v);
-              tmem_ld_wait();
+          for (int c = 0; c < HD / 32; ++c) {
+            uint32_t v[32];
+            tmem_ld32(tO(x) + lane_off + c * 32, v);
+            tmem_ld_wait();
 #pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * alpha);
-              tmem_st32(tO(x) + lane_off + c * 32, v);
-            }
+            for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * alpha);
+            tmem_st32(tO(x) + lane_off + c * 32, v);
           }
         }
         const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m_used, -m_used);

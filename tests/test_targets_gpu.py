@@ -119,12 +119,12 @@ def test_attention_matches_torch(shape):
     assert bool((err <= 2e-3 + 1e-2 * ref.abs()).all()), f"max err {err.max().item()}"
 
 
-def _attn_check(B, H, S, tol_abs=2e-3):
+def _attn_check(B, H, S, tol_abs=2e-3, sigma=0.5):
     """Run the shipped attention (nvcc schedule) and compare every head against fp32
     torch; the tolerance covers fp16 inputs of P and O: |d| <= tol_abs + 1e-2 |ref|."""
     from paper_2403_16863_b200.attention import AttnTarget
 
-    tgt = AttnTarget(B=B, H=H, S=S).allocate()
+    tgt = AttnTarget(B=B, H=H, S=S, sigma=sigma).allocate()
     be = B200Backend(tgt, paired=False)
     be.run_perm(None)
     torch.cuda.synchronize()
@@ -150,6 +150,16 @@ def _attn_check(B, H, S, tol_abs=2e-3):
 def test_attention_matches_torch_multi_item(shape):
     worst, grid, items = _attn_check(*shape)
     assert items > grid  # persistent: several items per CTA (carried rings, phases, o_free)
+
+
+@pytest.mark.parametrize("shape,sigma", [((1, 8, 1024), 2.0), ((1, 8, 1024), 3.0), ((1, 8, 1024), 8.0),
+                                         ((2, 4, 4096), 3.0)])
+def test_attention_large_scores_rescale_path(shape, sigma):
+    """Inputs of larger magnitude: row maxima keep growing past the lazy-rescale threshold,
+    so O is rescaled in many steps, by some rows of a warp and not others.  The rescale's
+    TMEM loads/stores are warp-collective; a per-lane guard around them hung the kernel
+    here (sigma >= 2).  Tolerance scaled with the output magnitude (~sigma)."""
+    worst, grid, items = _attn_check(*shape, tol_abs=2e-3 * sigma * sigma, sigma=sigma)
 
 
 def test_attention_matches_torch_with_few_ctas(monkeypatch):
