@@ -68,7 +68,10 @@ def test_patched_text_is_what_runs():
     assert not torch.equal(y3, want), "patched .text did not execute (loader used another copy)"
 
 
-@pytest.mark.parametrize("shape", [(256, 512, 256, 3), (512, 256, 1024, 1), (4096, 4096, 4096, 1)])
+@pytest.mark.parametrize("shape", [(256, 512, 256, 3), (512, 256, 1024, 1), (4096, 4096, 4096, 1),
+                                   (256, 256, 64, 1),      # one tile pair, one k-block
+                                   (768, 1280, 192, 2),    # odd tile counts, batched
+                                   (8192, 256, 64, 1)])    # a single tile column, many rows
 def test_gemm_lrelu_matches_torch(shape):
     M, N, K, L = shape
     tgt = GemmTarget(M=M, N=N, K=K, L=L).allocate()
@@ -150,6 +153,12 @@ def _attn_check(B, H, S, tol_abs=2e-3, sigma=0.5):
 def test_attention_matches_torch_multi_item(shape):
     worst, grid, items = _attn_check(*shape)
     assert items > grid  # persistent: several items per CTA (carried rings, phases, o_free)
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 256), (1, 3, 768), (3, 5, 1280)])
+def test_attention_small_and_odd_shapes(shape):
+    """Two K/V steps in one item; query-tile pairs and heads that do not divide the grid."""
+    _attn_check(*shape)
 
 
 @pytest.mark.parametrize("shape,sigma", [((1, 8, 1024), 2.0), ((1, 8, 1024), 3.0), ((1, 8, 1024), 8.0),
