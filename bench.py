@@ -659,7 +659,7 @@ def hardware_phase(kind, listing, local, rank, world, dist, args, rounds, shape=
                   "seconds": vsec, "samples_per_s": tot[0] / vsec,
                   "compare_gb_per_s": tot[4] / vsec / 1e9, "ranks": world,
                   "sample": ("one independent 256x256x1024 GEMM+LeakyReLU problem" if kind == "gemm"
-                             else "one independent head, S=512 D=128") + ", Philox inputs; baseline "
+                             else "one independent head, S=512 D=128, input scale cycling 0.5/1/2/4 over batches") + ", Philox inputs; baseline "
                             "and champion launched on it, outputs compared (sip_compare)",
                   "tolerance": {"atol": ver.atol, "rtol": ver.rtol}}
         # the same comparison at the tuned shape itself (one sample = one full problem of the

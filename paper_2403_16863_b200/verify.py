@@ -66,6 +66,9 @@ class VerifyResult:
         return {k: getattr(self, k) for k in self.__dataclass_fields__} | {"ok": self.ok}
 
 
+ATTN_SIGMAS = (0.5, 1.0, 2.0, 4.0)  # input scales attention batches cycle through
+
+
 class Verifier:
     """Baseline vs candidate over many samples for one target kind."""
 
@@ -91,6 +94,10 @@ class Verifier:
         self.launch_cand, self._p2 = self.target.launch(out=self.out_cand)
         self.elems_per_sample = self.out_ref.numel() // self.batch
         self.atol, self.rtol = TOLERANCE["fp16"]
+        # attention has a data-dependent path (the lazy O rescale when a row's max grows):
+        # batches cycle through input scales so that samples take it in many steps, not
+        # only at an item's first; a batch's scale is a function of its index (sharding-safe)
+        self.sigmas = ATTN_SIGMAS if kind == "attn" else None
 
     def _run(self, perm, launch) -> None:
         lib = self.ctx.lib
@@ -121,6 +128,8 @@ class Verifier:
         try:
             for i in range(nb):
                 j = first_batch + i * batch_stride
+                if self.sigmas:
+                    self.target.sigma = self.sigmas[j % len(self.sigmas)]
                 self.target.fill(stream=j)
                 self._check_run(lib.sip_run_async(self.module.handle, None, ctypes.byref(self.launch_ref)))
                 self._check_run(lib.sip_run_async(self.module.handle, pp, ctypes.byref(self.launch_cand)))

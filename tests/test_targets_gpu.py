@@ -187,8 +187,9 @@ def test_attention_listing_and_verifier():
     names = {ins.base_mnemonic for ins in L.kernel.schedule}
     assert {"UTCHMMA", "UTMALDG", "LDTM", "STG", "MUFU"} <= names
     assert len(candidates(L.kernel)) >= 4  # the epilogue STG.128s (+ the generic TMEM-slot load)
-    res = ver.run(np.arange(L.n, dtype=np.uint16), 128)
-    assert res.ok and res.bitdiff_elems == 0 and res.samples == 128
+    res = ver.run(np.arange(L.n, dtype=np.uint16), 256)  # four batches: input scales 0.5, 1, 2, 4
+    assert res.ok and res.bitdiff_elems == 0 and res.samples == 256
+    assert ver.target.sigma == ver.sigmas[-1] == 4.0
 
 
 def test_gemm_verifier_detects_a_broken_schedule():
